@@ -1,0 +1,256 @@
+// extern "C" implementation of include/bitdelta/capi.h. No exception crosses
+// the ABI: every entry point maps bd::Failure to its status code and stores the
+// message for bd_last_error(); CUDA errors map to BD_ERR_CUDA.
+#include <atomic>
+#include <cstring>
+#include <map>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+struct bd_pool;
+
+namespace bd {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+}  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+[[noreturn]] void fail(int code, const std::string& msg) { throw Failure{code, msg}; }
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw Failure{BD_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+// pool.cu
+bd_pool* pool_create(const bd_arch& a, int device, int world, int rank);
+void pool_destroy(bd_pool* p);
+void pool_set_tensor(bd_pool* p, const char* name, const void* data, bd_dtype dt, int is_dev,
+                     uint64_t rows, uint64_t cols);
+void pool_register(bd_pool* p, const char* id, const bd_delta_entry* e, int n);
+void pool_register_file(bd_pool* p, const char* id, const char* path, int resident);
+uint64_t pool_open(bd_pool* p, const char* id);
+void pool_close(bd_pool* p, uint64_t rid);
+void pool_decode(bd_pool* p, const bd_request* r, uint64_t n, int mode, float* logits, void* s);
+void pool_decode_layers(bd_pool* p, const bd_request* r, uint64_t n, const float* xin, float* xout,
+                        void* s);
+void pool_stats(const bd_pool* p, bd_pool_stats* out);
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return BD_OK;
+    } catch (const Failure& e) {
+        set_error(e.msg);
+        return e.code;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return BD_ERR_CUDA;
+    }
+}
+
+// ---- bd_multitenant_linear: K2 (tcgen05) + K3 (tenant-segmented) + combine ----
+struct LinearScratch {
+    float* P = nullptr;
+    size_t P_cap = 0;
+    float* D = nullptr;
+    size_t D_cap = 0;
+};
+
+void multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int32_t n_tenants,
+                        const uint8_t* const* tenant_bits, const float* tenant_alpha,
+                        int32_t batch, const int32_t* req_tenant, const void* X, float* Y,
+                        cudaStream_t stream) {
+    require(W && X && Y, BD_ERR_BAD_ARGUMENT, "multitenant_linear: null pointer");
+    require(batch >= 1 && batch <= 256, BD_ERR_BAD_ARGUMENT, "multitenant_linear: batch must be 1..256");
+    require(in_dim % 8 == 0, BD_ERR_BAD_ARGUMENT, "multitenant_linear: in_dim must be a multiple of 8");
+    require(out_dim >= 1 && out_dim < (1ull << 31), BD_ERR_BAD_ARGUMENT, "multitenant_linear: bad out_dim");
+    for (int b = 0; b < batch; ++b)
+        require(req_tenant == nullptr || req_tenant[b] < n_tenants, BD_ERR_UNKNOWN_ID,
+                "multitenant_linear: request tenant out of range");
+    const GemmPlan g = plan_base_gemm(out_dim, in_dim, batch);
+    const CUtensorMap mw = tmap_weights(W, out_dim, in_dim, in_dim);
+    const CUtensorMap mx = tmap_acts(X, batch, in_dim, in_dim, g.bn);
+    float* P = nullptr;
+    float* D = nullptr;
+    BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&P), sizeof(float) * g.splits * batch * out_dim, stream));
+    BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&D), sizeof(float) * batch * out_dim, stream));
+    base_gemm_launch(g, mw, mx, P, stream);
+    // tenant segmentation: each tenant's plane once for all of its requests
+    std::vector<DeltaUnit> units;
+    std::map<int, std::vector<int>> by_t;
+    std::vector<int> order;
+    for (int b = 0; b < batch; ++b) {
+        const int t = req_tenant ? req_tenant[b] : -1;
+        if (t < 0) continue;
+        require(tenant_bits && tenant_alpha && tenant_bits[t], BD_ERR_BAD_ARGUMENT,
+                "multitenant_linear: missing tenant bits");
+        if (!by_t.count(t)) order.push_back(t);
+        by_t[t].push_back(b);
+    }
+    for (int t : order) {
+        const auto& rq = by_t[t];
+        for (size_t c = 0; c < rq.size(); c += kMaxReqPerUnit) {
+            DeltaUnit u{};
+            u.n_planes = 1;
+            u.bits[0] = tenant_bits[t];
+            u.alpha[0] = tenant_alpha[t];
+            u.row0 = 0;
+            u.rows = int(out_dim);
+            u.n_req = int(std::min<size_t>(kMaxReqPerUnit, rq.size() - c));
+            for (int q = 0; q < u.n_req; ++q) u.req[q] = rq[c + q];
+            units.push_back(u);
+        }
+    }
+    delta_units_launch(units.data(), int(units.size()), X, int(in_dim), int(in_dim), batch, D,
+                       int(out_dim), stream);
+    combine_launch(P, g.splits, D, batch, int(out_dim), Y, stream);
+    BD_CUDA(cudaFreeAsync(P, stream));
+    BD_CUDA(cudaFreeAsync(D, stream));
+}
+
+}  // namespace bd
+
+using namespace bd;
+
+extern "C" {
+
+int bd_abi_version(void) { return BD_ABI_VERSION; }
+const char* bd_last_error(void) { return g_last_error.c_str(); }
+uint64_t bd_launch_count(void) { return launch_count(); }
+
+int bd_device_check(int device) {
+    return guarded([&] {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) fail(BD_ERR_NO_DEVICE, "no CUDA device");
+        require(device >= 0 && device < n, BD_ERR_NO_DEVICE, "device index out of range");
+        cudaDeviceProp p;
+        BD_CUDA(cudaGetDeviceProperties(&p, device));
+        require(p.major == 10 && p.minor == 0, BD_ERR_UNSUPPORTED_DEVICE,
+                std::string("libbitdelta_b200 is built for sm_100a; device is ") + p.name + " (sm_" +
+                    std::to_string(p.major) + std::to_string(p.minor) + ")");
+    });
+}
+
+uint64_t bd_packed_size(uint64_t rows, uint64_t cols) { return (rows * cols + 7) / 8; }
+
+int bd_compress(const void* base, const void* fine, bd_dtype dtype, uint64_t rows, uint64_t cols,
+                uint8_t* bits, float* alpha, void* stream) {
+    return guarded([&] {
+        bd_compress_job j{base, fine, rows, cols, bits, alpha};
+        compress_launch(&j, 1, dtype, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int bd_compress_batched(const bd_compress_job* jobs, int n_jobs, bd_dtype dtype, void* stream) {
+    return guarded([&] {
+        require(jobs != nullptr || n_jobs == 0, BD_ERR_BAD_ARGUMENT, "compress_batched: null jobs");
+        require(n_jobs >= 0, BD_ERR_BAD_ARGUMENT, "compress_batched: negative job count");
+        if (n_jobs) compress_launch(jobs, n_jobs, dtype, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int bd_compress_stack(const void* base, const void* fine, bd_dtype dtype, uint64_t rows,
+                      uint64_t cols, uint64_t planes, uint8_t* bits, float* alphas, void* stream) {
+    return guarded([&] {
+        require(fine && bits && alphas, BD_ERR_BAD_ARGUMENT, "compress_stack: null pointer");
+        compress_stack_launch(base, fine, dtype, rows, cols, planes, bits, alphas,
+                              static_cast<cudaStream_t>(stream));
+    });
+}
+
+int bd_packed_signed_accumulate(const uint8_t* bits, uint64_t rows, uint64_t cols, const float* x,
+                                uint64_t n_vec, float* out, void* stream) {
+    return guarded([&] {
+        packed_accumulate_launch(bits, rows, cols, x, n_vec, out, 1.0f, false,
+                                 static_cast<cudaStream_t>(stream));
+    });
+}
+
+int bd_packed_matvec(const uint8_t* bits, float alpha, uint64_t rows, uint64_t cols,
+                     const float* x, uint64_t n_vec, float* y, void* stream) {
+    return guarded([&] {
+        packed_accumulate_launch(bits, rows, cols, x, n_vec, y, alpha, true,
+                                 static_cast<cudaStream_t>(stream));
+    });
+}
+
+int bd_multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int32_t n_tenants,
+                          const uint8_t* const* tenant_bits, const float* tenant_alpha,
+                          int32_t batch, const int32_t* req_tenant, const void* X, float* Y,
+                          void* stream) {
+    return guarded([&] {
+        multitenant_linear(W, out_dim, in_dim, n_tenants, tenant_bits, tenant_alpha, batch,
+                           req_tenant, X, Y, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int bd_pool_create(const bd_arch* arch, int device, int world_size, int rank, bd_pool** out) {
+    return guarded([&] {
+        require(arch && out, BD_ERR_BAD_ARGUMENT, "pool_create: null argument");
+        *out = pool_create(*arch, device, world_size, rank);
+    });
+}
+void bd_pool_destroy(bd_pool* pool) {
+    if (pool) pool_destroy(pool);
+}
+int bd_pool_set_tensor(bd_pool* pool, const char* name, const void* data, bd_dtype dtype,
+                       int is_device, uint64_t rows, uint64_t cols) {
+    return guarded([&] {
+        require(pool != nullptr, BD_ERR_BAD_ARGUMENT, "null pool");
+        pool_set_tensor(pool, name, data, dtype, is_device, rows, cols);
+    });
+}
+int bd_pool_register_delta(bd_pool* pool, const char* id, const bd_delta_entry* entries,
+                           int n_entries) {
+    return guarded([&] {
+        require(pool != nullptr, BD_ERR_BAD_ARGUMENT, "null pool");
+        pool_register(pool, id, entries, n_entries);
+    });
+}
+int bd_pool_register_delta_file(bd_pool* pool, const char* id, const char* path, int resident) {
+    return guarded([&] {
+        require(pool != nullptr, BD_ERR_BAD_ARGUMENT, "null pool");
+        pool_register_file(pool, id, path, resident);
+    });
+}
+int bd_pool_open_request(bd_pool* pool, const char* delta_id, uint64_t* request_id) {
+    return guarded([&] {
+        require(pool && request_id, BD_ERR_BAD_ARGUMENT, "null argument");
+        *request_id = pool_open(pool, delta_id);
+    });
+}
+int bd_pool_close_request(bd_pool* pool, uint64_t request_id) {
+    return guarded([&] {
+        require(pool != nullptr, BD_ERR_BAD_ARGUMENT, "null pool");
+        pool_close(pool, request_id);
+    });
+}
+int bd_pool_decode_step(bd_pool* pool, const bd_request* reqs, uint64_t n, int mode,
+                        float* logits, void* stream) {
+    return guarded([&] {
+        require(pool != nullptr, BD_ERR_BAD_ARGUMENT, "null pool");
+        pool_decode(pool, reqs, n, mode, logits, stream);
+    });
+}
+int bd_pool_decode_layers(bd_pool* pool, const bd_request* reqs, uint64_t n, const float* x_in,
+                          float* x_out, void* stream) {
+    return guarded([&] {
+        require(pool != nullptr, BD_ERR_BAD_ARGUMENT, "null pool");
+        pool_decode_layers(pool, reqs, n, x_in, x_out, stream);
+    });
+}
+int bd_pool_get_stats(const bd_pool* pool, bd_pool_stats* out) {
+    return guarded([&] {
+        require(pool && out, BD_ERR_BAD_ARGUMENT, "null argument");
+        pool_stats(pool, out);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,259 @@
+// K2 — shared base contraction on the 5th-gen tensor cores (replaces
+// deltakit::matmul_nt, P:src/matrix.cpp:26-41, as called by
+// ServingPool::backbone_linear_nt, P:src/serve.cpp:120-127).
+//
+//   P[split][n][m] = sum_{k in split} W[m][k] * X[n][k]     (bf16 in, f32 out)
+//
+// Swap-AB: the weight rows are the MMA M dimension (128 per CTA tile) and the
+// decode batch is N (16..256), so a batch of 16 costs one 128x16 MMA per
+// 16-wide K step. Operands are staged by TMA (128-byte swizzle) through an
+// mbarrier ring; one elected thread issues tcgen05.mma into a TMEM
+// accumulator; all four warps drain TMEM with tcgen05.ld. Split-K partials are
+// written, not atomically added, so results are bit-reproducible and
+// independent of the order of requests in the batch (test_serve.cpp:169-190).
+//
+// Roofline: HBM — 2 bytes per weight element; at batch B the intensity is B
+// flop/byte, far below the tensor pipe's ridge point.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace bd {
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;  // bf16 elements = 128 bytes = one swizzle row
+constexpr int kMaxStages = 8;
+constexpr int kGemmThreads = 128;
+
+struct GemmSmemLayout {
+    uint32_t a_bytes, b_bytes, stage_bytes, stages, total;
+};
+
+__host__ __device__ inline GemmSmemLayout gemm_layout(int bn, int stages) {
+    GemmSmemLayout L;
+    L.a_bytes = kBM * kBK * 2;
+    L.b_bytes = bn * kBK * 2;
+    L.stage_bytes = L.a_bytes + L.b_bytes;
+    L.stages = stages;
+    L.total = 1024 /*align slack*/ + stages * L.stage_bytes + 256 /*barriers*/;
+    return L;
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    base_gemm_kernel(const __grid_constant__ CUtensorMap map_w,
+                     const __grid_constant__ CUtensorMap map_x, float* __restrict__ partial,
+                     int M, int N_valid, int bn, int kb_total, int kb_per_split, int stages) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    const GemmSmemLayout L = gemm_layout(bn, stages);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * L.stage_bytes);
+    uint64_t* empty = full + kMaxStages;
+    uint64_t* done = empty + kMaxStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    const int m0 = blockIdx.x * kBM;
+    const int split = blockIdx.y;
+    const int kb0 = split * kb_per_split;
+    const int kb1 = min(kb_total, kb0 + kb_per_split);
+    const int nkb = kb1 - kb0;
+    const uint32_t tmem_cols_needed = bn <= 32 ? 32 : (bn <= 64 ? 64 : (bn <= 128 ? 128 : 256));
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&map_w);
+        prefetch_tmap(&map_x);
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(done, 1);
+        fence_mbar_init();
+    }
+    if (warp == 2) {
+        // allocation size must be a compile-time immediate
+        if (tmem_cols_needed == 32) tmem_alloc<32>(tmem_slot);
+        else if (tmem_cols_needed == 64) tmem_alloc<64>(tmem_slot);
+        else if (tmem_cols_needed == 128) tmem_alloc<128>(tmem_slot);
+        else tmem_alloc<256>(tmem_slot);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t taddr = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ---- TMA producer ----
+        const uint64_t pol_w = policy_evict_first();  // weights stream once per step
+        for (int i = 0; i < nkb; ++i) {
+            const int s = i % stages;
+            const uint32_t round = i / stages;
+            mbar_wait(&empty[s], (round & 1) ^ 1);
+            uint8_t* a = smem + s * L.stage_bytes;
+            uint8_t* b = a + L.a_bytes;
+            mbar_arrive_expect_tx(&full[s], L.stage_bytes);
+            const int kc = (kb0 + i) * kBK;
+            tma_load_2d_hint(a, &map_w, &full[s], kc, m0, pol_w);
+            tma_load_2d(b, &map_x, &full[s], kc, 0);
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---- MMA issuer ----
+        const uint32_t idesc = idesc_bf16_f32(kBM, bn);
+        for (int i = 0; i < nkb; ++i) {
+            const int s = i % stages;
+            const uint32_t round = i / stages;
+            mbar_wait(&full[s], round & 1);
+            tc_fence_after();
+            uint8_t* a = smem + s * L.stage_bytes;
+            uint8_t* b = a + L.a_bytes;
+            const uint64_t da = sdesc_k128(a), db = sdesc_k128(b);
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k)  // +32 bytes per 16-wide K step
+                mma_bf16_ss(taddr, da + 2 * k, db + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
+            tc_commit(&empty[s]);
+        }
+        tc_commit(done);
+    }
+
+    // ---- epilogue: all 4 warps drain their 32 TMEM lanes ----
+    __syncwarp();
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const int row = m0 + warp * 32 + lane;
+    float* out = partial + static_cast<size_t>(split) * N_valid * M;
+    for (int c0 = 0; c0 < bn; c0 += 16) {
+        uint32_t r[16];
+        tmem_ld16(taddr + ((warp * 32) << 16) + c0, r);
+        tmem_ld_wait();
+        if (nkb <= 0) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) r[j] = 0;
+        }
+        if (row < M) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int n = c0 + j;
+                if (n < N_valid) out[static_cast<size_t>(n) * M + row] = __uint_as_float(r[j]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        if (tmem_cols_needed == 32) tmem_dealloc<32>(taddr);
+        else if (tmem_cols_needed == 64) tmem_dealloc<64>(taddr);
+        else if (tmem_cols_needed == 128) tmem_dealloc<128>(taddr);
+        else tmem_dealloc<256>(taddr);
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        BD_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        require(p != nullptr && q == cudaDriverEntryPointSuccess, BD_ERR_CUDA,
+                "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+}  // namespace
+
+void note_launch();
+
+// 2-D row-major [rows x cols] tensor, box {box_cols, box_rows}, 128B swizzle.
+CUtensorMap make_tmap_2d(const void* ptr, CUtensorMapDataType dt, uint32_t elem_bytes,
+                         uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
+                         uint32_t box_rows, uint32_t box_cols, bool swizzle128) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {row_stride_elems * elem_bytes};
+    const cuuint32_t box[2] = {box_cols, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    require((strides[0] % 16) == 0, BD_ERR_BAD_ARGUMENT,
+            "TMA: row stride must be a multiple of 16 bytes");
+    require((reinterpret_cast<uintptr_t>(ptr) % 16) == 0, BD_ERR_BAD_ARGUMENT,
+            "TMA: base pointer must be 16-byte aligned");
+    const CUresult r = encode_fn()(&m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                              : CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    require(r == CUDA_SUCCESS, BD_ERR_CUDA,
+            "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    return m;
+}
+
+GemmPlan plan_base_gemm(uint64_t M, uint64_t K, int batch, int ctas_per_sm_hint) {
+    GemmPlan p;
+    p.M = M;
+    p.K = K;
+    p.batch = batch;
+    p.bn = std::max(16, ((batch + 15) / 16) * 16);
+    require(p.bn <= 256, BD_ERR_BAD_ARGUMENT, "base gemm: batch chunk must be <= 256");
+    const GemmSmemLayout L0 = gemm_layout(p.bn, 1);
+    // as many stages as fit in ~200 KB (2 CTAs/SM when the stage is small)
+    int stages = std::min(kMaxStages, int((200 * 1024 - 1024 - 256) / L0.stage_bytes));
+    const bool two_per_sm = (gemm_layout(p.bn, 4).total * 2 <= 227 * 1024);
+    if (two_per_sm) stages = std::min(stages, int((110 * 1024 - 1280) / L0.stage_bytes));
+    p.stages = std::max(2, stages);
+    p.smem = gemm_layout(p.bn, p.stages).total;
+    const int slots = kNumSMs * (two_per_sm ? 2 : 1) * std::max(1, ctas_per_sm_hint);
+    const int m_tiles = int((M + kBM - 1) / kBM);
+    const int kb = int((K + kBK - 1) / kBK);
+    // split-K to fill the machine: minimise ceil(tiles*s/slots) * ceil(kb/s)
+    int best_s = 1;
+    double best_cost = 1e30;
+    for (int s = 1; s <= std::min(kb, 32); ++s) {
+        const int per = (kb + s - 1) / s;
+        const int s_eff = (kb + per - 1) / per;
+        const double waves = std::ceil(double(m_tiles) * s_eff / slots);
+        const double cost = waves * (per + 2.0 /*fixed per-CTA overhead in k-blocks*/);
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best_s = s_eff;
+        }
+    }
+    p.kb_total = kb;
+    p.kb_per_split = (kb + best_s - 1) / best_s;
+    p.splits = (kb + p.kb_per_split - 1) / p.kb_per_split;
+    p.m_tiles = m_tiles;
+    return p;
+}
+
+void base_gemm_launch(const GemmPlan& p, const CUtensorMap& map_w, const CUtensorMap& map_x,
+                      float* partial, cudaStream_t stream) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        BD_CUDA(cudaFuncSetAttribute(base_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     227 * 1024));
+        attr_set = true;
+    }
+    dim3 grid(p.m_tiles, p.splits);
+    base_gemm_kernel<<<grid, kGemmThreads, p.smem, stream>>>(
+        map_w, map_x, partial, int(p.M), p.batch, p.bn, p.kb_total, p.kb_per_split, p.stages);
+    note_launch();
+    BD_CUDA(cudaGetLastError());
+}
+
+CUtensorMap tmap_weights(const void* W, uint64_t M, uint64_t K, uint64_t ld) {
+    return make_tmap_2d(W, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, K, ld, kBM, kBK, true);
+}
+CUtensorMap tmap_acts(const void* X, int batch, uint64_t K, uint64_t ld, int bn) {
+    return make_tmap_2d(X, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, uint64_t(batch), K, ld,
+                        uint32_t(bn), kBK, true);
+}
+
+}  // namespace bd

@@ -1,0 +1,248 @@
+// K4 — decode-layer glue of ServingPool::decode_shared (P:src/serve.cpp:224-321)
+// with the reference's numerics (P:include/deltakit/nn_ops.hpp:15-59):
+//   * RMSNorm with double statistics and eps 1e-12 (nn_ops.hpp:15-25), the
+//     per-tenant weight being backbone row + raw delta row (serve.cpp:224-228);
+//   * interleaved-pair RoPE (nn_ops.hpp:29-45) from a host-built table whose
+//     cos/sin come from the same double pow/cos/sin the reference evaluates;
+//   * f32 softmax (nn_ops.hpp:48-57) and SiLU (nn_ops.hpp:59).
+// Each glue kernel also folds in the split-K reduction of the projection that
+// produced its input (sum of base partials + tenant delta), so the linears
+// never make an extra pass over their outputs.
+#include <algorithm>
+
+#include "common.cuh"
+#include "glue.h"
+
+namespace bd {
+
+void note_launch();
+
+namespace {
+
+__device__ __forceinline__ float proj_val(const ProjOut& p, int b, int m) {
+    float s = 0.0f;
+    for (int k = 0; k < p.splits; ++k) s += p.P[static_cast<size_t>(k) * p.pstride + size_t(b) * p.M + m];
+    if (p.D) s += p.D[size_t(b) * p.M + m];
+    return s;
+}
+
+__device__ __forceinline__ uint16_t f32_to_bf16(float v) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(v));
+}
+
+template <typename T>
+__device__ T block_sum(T v, T* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    T t = 0;
+    for (int i = 0; i < nw; ++i) t += red[i];
+    return t;
+}
+__device__ float block_max(float v, float* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    float t = red[0];
+    for (int i = 1; i < nw; ++i) t = fmaxf(t, red[i]);
+    return t;
+}
+
+// one block per request: x += proj (optional); xn = rmsnorm(x) * w_b (optional)
+__global__ void resid_norm_kernel(float* __restrict__ x, int dim, ProjOut proj,
+                                  const float* const* __restrict__ norm_w,
+                                  uint16_t* __restrict__ xn, int ldxn, float* __restrict__ xn_f32) {
+    __shared__ double red_d[32];
+    const int b = blockIdx.x;
+    float* xb = x + size_t(b) * dim;
+    double msq = 0.0;
+    for (int i = threadIdx.x; i < dim; i += blockDim.x) {
+        float v = xb[i];
+        if (proj.P) {
+            v = v + proj_val(proj, b, proj.col0 + i);
+            xb[i] = v;
+        }
+        msq += static_cast<double>(v) * v;
+    }
+    if (!norm_w) return;
+    msq = block_sum(msq, red_d);
+    const double inv = 1.0 / sqrt(msq / static_cast<double>(dim) + 1e-12);
+    const float* w = norm_w[b];
+    for (int i = threadIdx.x; i < dim; i += blockDim.x) {
+        const float y = static_cast<float>(static_cast<double>(xb[i]) * inv) * w[i];
+        if (xn) xn[size_t(b) * ldxn + i] = f32_to_bf16(y);
+        if (xn_f32) xn_f32[size_t(b) * dim + i] = y;
+    }
+}
+
+// one block per (head, request)
+__global__ void attn_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos_dev,
+                            uint16_t* __restrict__ ctx_out, int ld_ctx) {
+    extern __shared__ float sm[];
+    float* qs = sm;                 // hd
+    float* ks = qs + a.hd;          // hd (this step's key, bf16-rounded)
+    float* vs = ks + a.hd;          // hd
+    float* scores = vs + a.hd;      // max_seq
+    __shared__ float red[32];
+    const int h = blockIdx.x, b = blockIdx.y;
+    const int hd = a.hd, half = hd / 2;
+    const int group = a.n_heads / a.n_kv_heads;
+    const int kh = h / group;
+    const int pos = pos_dev[b];
+    const float2* rope = a.rope + static_cast<size_t>(pos) * half;
+
+    // q, k, v of this step (split-K reduction + tenant delta), RoPE on q and k
+    for (int i = threadIdx.x; i < half; i += blockDim.x) {
+        const float2 cs = rope[i];
+        const float q0 = proj_val(qkv, b, h * hd + 2 * i), q1 = proj_val(qkv, b, h * hd + 2 * i + 1);
+        qs[2 * i] = q0 * cs.x - q1 * cs.y;
+        qs[2 * i + 1] = q0 * cs.y + q1 * cs.x;
+        const int kc = a.dim + kh * hd;
+        const float k0 = proj_val(qkv, b, kc + 2 * i), k1 = proj_val(qkv, b, kc + 2 * i + 1);
+        ks[2 * i] = bf16_to_f32(f32_to_bf16(k0 * cs.x - k1 * cs.y));
+        ks[2 * i + 1] = bf16_to_f32(f32_to_bf16(k0 * cs.y + k1 * cs.x));
+    }
+    for (int i = threadIdx.x; i < hd; i += blockDim.x)
+        vs[i] = bf16_to_f32(f32_to_bf16(proj_val(qkv, b, a.dim + a.kv_dim + kh * hd + i)));
+    __syncthreads();
+    uint16_t* kc = a.kcache[b] + (static_cast<size_t>(a.layer) * a.max_seq) * a.kv_dim + kh * hd;
+    uint16_t* vc = a.vcache[b] + (static_cast<size_t>(a.layer) * a.max_seq) * a.kv_dim + kh * hd;
+    if (h % group == 0) {  // KV append (serve.cpp:261-264), post-RoPE
+        for (int i = threadIdx.x; i < hd; i += blockDim.x) {
+            kc[static_cast<size_t>(pos) * a.kv_dim + i] = f32_to_bf16(ks[i]);
+            vc[static_cast<size_t>(pos) * a.kv_dim + i] = f32_to_bf16(vs[i]);
+        }
+    }
+    // scores (serve.cpp:267-275): one warp per key
+    const int n_ctx = pos + 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const float inv_sqrt_hd = 1.0f / sqrtf(static_cast<float>(hd));
+    for (int j = warp; j < n_ctx; j += nw) {
+        float acc = 0.0f;
+        if (j == pos) {
+            for (int d = lane; d < hd; d += 32) acc += qs[d] * ks[d];
+        } else {
+            const uint16_t* kj = kc + static_cast<size_t>(j) * a.kv_dim;
+            for (int d = lane; d < hd; d += 32) acc += qs[d] * bf16_to_f32(kj[d]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) scores[j] = acc * inv_sqrt_hd;
+    }
+    __syncthreads();
+    // softmax (nn_ops.hpp:48-57)
+    float mx = -INFINITY;
+    for (int j = threadIdx.x; j < n_ctx; j += blockDim.x) mx = fmaxf(mx, scores[j]);
+    mx = block_max(mx, red);
+    float sum = 0.0f;
+    for (int j = threadIdx.x; j < n_ctx; j += blockDim.x) {
+        const float e = expf(scores[j] - mx);
+        scores[j] = e;
+        sum += e;
+    }
+    sum = block_sum(sum, red);
+    __syncthreads();
+    // ctx (serve.cpp:276-281): sequential over positions, like the reference
+    for (int d = threadIdx.x; d < hd; d += blockDim.x) {
+        float acc = 0.0f;
+        for (int j = 0; j < n_ctx; ++j) {
+            const float v = (j == pos) ? vs[d] : bf16_to_f32(vc[static_cast<size_t>(j) * a.kv_dim + d]);
+            acc += (scores[j] / sum) * v;
+        }
+        ctx_out[size_t(b) * ld_ctx + h * hd + d] = f32_to_bf16(acc);
+    }
+}
+
+// act = silu(gate) * up (serve.cpp:301-302)
+__global__ void silu_kernel(ProjOut gu, int inter, uint16_t* __restrict__ act, int ld_act) {
+    const int b = blockIdx.y;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < inter; i += gridDim.x * blockDim.x) {
+        const float g = proj_val(gu, b, i);
+        const float u = proj_val(gu, b, inter + i);
+        const float s = g / (1.0f + expf(-g));
+        act[size_t(b) * ld_act + i] = f32_to_bf16(s * u);
+    }
+}
+
+// x[b] = embed[tok_b] + raw embed delta row (serve.cpp:230-236)
+__global__ void embed_kernel(const float* __restrict__ embed, const int* __restrict__ tokens,
+                             const float* const* __restrict__ embed_delta, int dim,
+                             float* __restrict__ x) {
+    const int b = blockIdx.x;
+    const size_t tok = static_cast<size_t>(tokens[b]);
+    const float* d = embed_delta ? embed_delta[b] : nullptr;
+    for (int i = threadIdx.x; i < dim; i += blockDim.x) {
+        float v = embed[tok * dim + i];
+        if (d) v += d[tok * dim + i];
+        x[size_t(b) * dim + i] = v;
+    }
+}
+
+// logits[b][r] = proj(b, r) + raw lm_head delta row . xn_f32[b]  (serve.cpp:316-320)
+__global__ void logits_kernel(ProjOut lm, const float* const* __restrict__ raw_delta,
+                              const float* __restrict__ xn_f32, int dim, int vocab,
+                              float* __restrict__ logits) {
+    const int b = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const float* rd = raw_delta ? raw_delta[b] : nullptr;
+    for (int r = blockIdx.x * (blockDim.x >> 5) + warp; r < vocab; r += gridDim.x * (blockDim.x >> 5)) {
+        float acc = 0.0f;
+        if (rd)
+            for (int c = lane; c < dim; c += 32) acc += rd[size_t(r) * dim + c] * xn_f32[size_t(b) * dim + c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) logits[size_t(b) * vocab + r] = proj_val(lm, b, r) + acc;
+    }
+}
+
+}  // namespace
+
+void resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const float* const* norm_w,
+                       uint16_t* xn, int ldxn, float* xn_f32, cudaStream_t s) {
+    resid_norm_kernel<<<batch, 256, 0, s>>>(x, dim, proj, norm_w, xn, ldxn, xn_f32);
+    note_launch();
+    BD_CUDA(cudaGetLastError());
+}
+
+void attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int batch,
+                 uint16_t* ctx, int ld_ctx, cudaStream_t s) {
+    const size_t smem = (3 * a.hd + a.max_seq) * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+        BD_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    attn_kernel<<<dim3(a.n_heads, batch), 128, smem, s>>>(qkv, a, pos_dev, ctx, ld_ctx);
+    note_launch();
+    BD_CUDA(cudaGetLastError());
+}
+
+void silu_launch(const ProjOut& gu, int batch, int inter, uint16_t* act, int ld_act, cudaStream_t s) {
+    const int bx = std::max(1, std::min((inter + 255) / 256, 64));
+    silu_kernel<<<dim3(bx, batch), 256, 0, s>>>(gu, inter, act, ld_act);
+    note_launch();
+    BD_CUDA(cudaGetLastError());
+}
+
+void embed_launch(const float* embed, const int* tokens, const float* const* embed_delta, int batch,
+                  int dim, float* x, cudaStream_t s) {
+    embed_kernel<<<batch, 256, 0, s>>>(embed, tokens, embed_delta, dim, x);
+    note_launch();
+    BD_CUDA(cudaGetLastError());
+}
+
+void logits_launch(const ProjOut& lm, const float* const* raw_delta, const float* xn_f32, int batch,
+                   int dim, int vocab, float* logits, cudaStream_t s) {
+    const int bx = std::max(1, std::min((vocab + 7) / 8, 256));
+    logits_kernel<<<dim3(bx, batch), 256, 0, s>>>(lm, raw_delta, xn_f32, dim, vocab, logits);
+    note_launch();
+    BD_CUDA(cudaGetLastError());
+}
+
+}  // namespace bd

@@ -1,0 +1,37 @@
+// Host interface of the decode glue kernels (K4).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bd {
+
+// A projection's output as produced by K2/K3: value(b, m) =
+//   sum_{s < splits} P[s*pstride + b*M + m] + D[b*M + m]   (D may be null).
+struct ProjOut {
+    const float* P = nullptr;
+    int splits = 0;
+    size_t pstride = 0;
+    const float* D = nullptr;
+    int M = 0;
+    int col0 = 0;  // column offset used by resid_norm (o / down outputs)
+};
+
+struct AttnArgs {
+    int dim, kv_dim, n_heads, n_kv_heads, hd, max_seq, layer;
+    uint16_t* const* kcache;  // per request: [n_layers][max_seq][kv_dim] bf16
+    uint16_t* const* vcache;
+    const float2* rope;       // [max_seq][hd/2] (cos, sin)
+};
+
+void resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const float* const* norm_w,
+                       uint16_t* xn, int ldxn, float* xn_f32, cudaStream_t s);
+void attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int batch,
+                 uint16_t* ctx, int ld_ctx, cudaStream_t s);
+void silu_launch(const ProjOut& gu, int batch, int inter, uint16_t* act, int ld_act, cudaStream_t s);
+void embed_launch(const float* embed, const int* tokens, const float* const* embed_delta, int batch,
+                  int dim, float* x, cudaStream_t s);
+void logits_launch(const ProjOut& lm, const float* const* raw_delta, const float* xn_f32, int batch,
+                   int dim, int vocab, float* logits, cudaStream_t s);
+
+}  // namespace bd

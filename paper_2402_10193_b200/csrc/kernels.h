@@ -1,0 +1,63 @@
+// Host-side interface of the kernels (K1..K4) shared by the C-ABI and engine.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "../../include/bitdelta/capi.h"
+
+namespace bd {
+
+// ---- K2 base GEMM ----
+struct GemmPlan {
+    uint64_t M = 0, K = 0;
+    int batch = 0, bn = 16, stages = 4, smem = 0;
+    int m_tiles = 0, kb_total = 0, kb_per_split = 0, splits = 1;
+};
+GemmPlan plan_base_gemm(uint64_t M, uint64_t K, int batch, int ctas_per_sm_hint = 1);
+CUtensorMap make_tmap_2d(const void* ptr, CUtensorMapDataType dt, uint32_t elem_bytes,
+                         uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
+                         uint32_t box_rows, uint32_t box_cols, bool swizzle128);
+CUtensorMap tmap_weights(const void* W, uint64_t M, uint64_t K, uint64_t ld);
+CUtensorMap tmap_acts(const void* X, int batch, uint64_t K, uint64_t ld, int bn);
+// partial: [splits][batch][M] f32
+void base_gemm_launch(const GemmPlan& p, const CUtensorMap& map_w, const CUtensorMap& map_x,
+                      float* partial, cudaStream_t stream);
+
+// ---- K1 compressor ----
+void compress_launch(const bd_compress_job* jobs, int n_jobs, bd_dtype dtype, cudaStream_t s);
+void compress_stack_launch(const void* base, const void* fine, bd_dtype dtype, uint64_t rows,
+                           uint64_t cols, uint64_t planes, uint8_t* bits, float* alphas,
+                           cudaStream_t stream);
+
+// ---- K3 drop-in (a7/a8) ----
+void packed_accumulate_launch(const uint8_t* bits, uint64_t rows, uint64_t cols, const float* x,
+                              uint64_t n_vec, float* out, float scale, bool overwrite,
+                              cudaStream_t stream);
+
+// ---- K3 multi-tenant delta ----
+// One delta "unit" = one sign plane of one tenant applied to the rows
+// [row0, row0+rows) of a (possibly stacked) projection output, for the
+// requests req[0..n_req). Output d[b][row] = sum over units of alpha * S x_b.
+constexpr int kMaxReqPerUnit = 4;
+constexpr int kMaxPlanesPerUnit = 4;
+struct DeltaUnit {
+    const uint8_t* bits[kMaxPlanesPerUnit];  // reference layout of one [rows x cols] plane each
+    float alpha[kMaxPlanesPerUnit];
+    int32_t n_planes;
+    int32_t row0, rows;  // output rows [row0, row0+rows) of the stacked projection
+    int32_t n_req;
+    int32_t req[kMaxReqPerUnit];
+};
+// X: bf16 [batch x ldx] activations; D: f32 [batch x out_rows] (zeroed here)
+void delta_units_launch(const DeltaUnit* units_host, int n_units, const void* X, int ldx,
+                        int cols, int batch, float* D, int out_rows, cudaStream_t stream);
+
+// Y[b][m] = sum_s P[s][b][m] (+ D[b][m])
+void combine_launch(const float* P, int splits, const float* D, int batch, int M, float* Y,
+                    cudaStream_t stream);
+
+}  // namespace bd

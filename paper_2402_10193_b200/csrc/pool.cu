@@ -1,0 +1,973 @@
+// Device-resident multi-tenant ServingPool — the B200 replacement of
+// deltakit::ServingPool (P:include/deltakit/serve.hpp:59-125,
+// P:src/serve.cpp:93-342).
+//
+// Layout in HBM (one process per GPU, rank r of world W holds rows
+// [r*R/W, (r+1)*R/W) of every projection; W = 1 on one GPU):
+//   * per layer, bf16 backbone linears stacked so one GEMM serves a group:
+//       Wqkv [q_l + 2 kv_l, dim]   Wo [dim_l, dim]   Wgu [2 inter_l, dim]
+//       Wdown [dim_l, inter]       (row stride padded to 8 elements for TMA)
+//   * per tenant, per layer and projection: the sign planes in the reference
+//     byte layout (one device buffer per plane, 16-byte aligned) + f32 alpha;
+//     effective norm rows (backbone + raw delta, serve.cpp:224-228) in f32;
+//   * per request: a bf16 KV cache [n_layers][max_seq][kv_dim] for k and v.
+// A decode step runs, per layer, K4 norm -> K2+K3 qkv -> K4 attention ->
+// K2+K3 o -> K4 residual+norm -> K2+K3 gate|up -> K4 silu -> K2+K3 down, with
+// the split-K/delta reduction folded into the next glue kernel. Requests are
+// segmented by tenant so each tenant's planes are streamed once per step.
+// Steps for a fixed batch composition are captured once into a CUDA graph
+// and replayed; only positions/tokens are re-uploaded per step.
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "bdelta_io.h"
+#include "common.cuh"
+#include "glue.h"
+#include "kernels.h"
+
+namespace bd {
+
+void note_launch();
+uint64_t launch_count();
+
+namespace {
+
+enum Proj { P_Q, P_K, P_V, P_O, P_GATE, P_UP, P_DOWN, P_COUNT };
+const char* kProjNames[P_COUNT] = {"attn_q", "attn_k", "attn_v", "attn_o",
+                                   "mlp_gate", "mlp_up", "mlp_down"};
+
+__global__ void f32_to_bf16_2d(const float* __restrict__ src, uint64_t rows, uint64_t cols,
+                               uint64_t lds, uint16_t* __restrict__ dst, uint64_t ldd) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < rows * cols;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t r = i / cols, c = i % cols;
+        dst[r * ldd + c] = __bfloat16_as_ushort(__float2bfloat16_rn(src[r * lds + c]));
+    }
+}
+
+uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
+
+template <typename T>
+T* dmalloc(size_t n, std::vector<void*>* owner = nullptr) {
+    void* p = nullptr;
+    BD_CUDA(cudaMalloc(&p, std::max<size_t>(n * sizeof(T), 16)));
+    if (owner) owner->push_back(p);
+    return static_cast<T*>(p);
+}
+
+struct Plane {
+    const uint8_t* bits;
+    float alpha;
+};
+
+struct Tenant {
+    std::string id, path;
+    bool resident = false, loaded = false;
+    // [layer][proj] -> planes (this rank's row slice)
+    std::vector<std::array<std::vector<Plane>, P_COUNT>> proj;
+    std::vector<float*> norm1, norm2;  // device, effective
+    float* final_norm = nullptr;
+    float* embed_raw = nullptr;        // device [vocab x dim] or null
+    float* lm_raw = nullptr;           // device [vocab x dim] or null
+    std::vector<Plane> lm_planes;      // packed lm_head (rank-local rows)
+    std::vector<void*> allocs;
+    uint64_t bytes = 0;                // payload bytes as accounted by the reference
+};
+
+struct Request {
+    int tenant = -1;
+    bool open = false;
+    uint64_t pos = 0;
+    uint16_t* kc = nullptr;
+    uint16_t* vc = nullptr;
+};
+
+struct LayerW {
+    uint16_t *qkv = nullptr, *o = nullptr, *gu = nullptr, *down = nullptr;
+    CUtensorMap m_qkv, m_o, m_gu, m_down;
+};
+
+struct Plan {
+    int B = 0;
+    std::vector<int> reqs;  // pool request indices
+    // device pointer tables
+    float** d_norm = nullptr;       // [(2L+1) * B]
+    uint16_t** d_kc = nullptr;      // [B]
+    uint16_t** d_vc = nullptr;
+    float** d_embed = nullptr;      // [B] or null
+    float** d_lmraw = nullptr;      // [B] or null
+    int* d_pos = nullptr;
+    int* d_tok = nullptr;
+    int* h_pos = nullptr;           // pinned
+    int* h_tok = nullptr;
+    std::vector<void*> allocs;
+    // per layer & group: delta units
+    std::vector<std::array<std::vector<DeltaUnit>, 4>> units;  // qkv, o, gu, down
+    std::vector<DeltaUnit> lm_units;
+    GemmPlan g_qkv, g_o, g_gu, g_down, g_lm;
+    CUtensorMap x_xn, x_ctx, x_act;  // B-operand maps for this batch size
+    cudaGraphExec_t graph_layers = nullptr, graph_full = nullptr;
+    uint64_t kernels_layers = 0, kernels_full = 0;
+};
+
+}  // namespace
+
+struct PoolImpl {
+    bd_arch a{};
+    int device = 0, world = 1, rank = 0;
+    uint64_t hd = 0, n_kv_heads = 0;
+    uint64_t q_l = 0, kv_l = 0, dim_l = 0, inter_l = 0;  // rank-local rows
+    uint64_t q_r0 = 0, kv_r0 = 0, dim_r0 = 0, inter_r0 = 0;
+    uint64_t ld_dim = 0, ld_inter = 0;  // padded strides (elements)
+    std::vector<LayerW> L;
+    std::vector<std::vector<float>> base_norm1, base_norm2;  // host copies (full)
+    std::vector<float> base_final_norm;
+    float* embed = nullptr;
+    uint16_t* lm_head = nullptr;
+    CUtensorMap m_lm;
+    std::vector<bool> have;  // tensor set flags (tensor_shapes order)
+    std::vector<void*> allocs;
+    float2* rope = nullptr;
+    uint64_t backbone_bytes = 0;
+
+    std::vector<Tenant> tenants;
+    std::map<std::string, int> tenant_idx;
+    std::vector<Request> requests;
+    bd_pool_stats stats{};
+
+    // workspaces (sized for ws_B)
+    int ws_B = 0;
+    float *x = nullptr, *xn_f32 = nullptr, *P = nullptr, *D = nullptr, *logits = nullptr;
+    uint16_t *xn = nullptr, *ctx = nullptr, *act = nullptr;
+    size_t P_elems = 0, D_elems = 0;
+    std::vector<void*> ws_allocs;
+
+    std::map<std::string, std::unique_ptr<Plan>> plans;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    bool use_graphs = true;
+
+    ~PoolImpl() {
+        cudaSetDevice(device);
+        if (stream) cudaStreamSynchronize(stream);
+        clear_plans();
+        free_ws();
+        for (auto& t : tenants) for (void* p : t.allocs) cudaFree(p);
+        for (auto& r : requests) { if (r.kc) cudaFree(r.kc); if (r.vc) cudaFree(r.vc); }
+        for (void* p : allocs) cudaFree(p);
+        if (ev_in) cudaEventDestroy(ev_in);
+        if (ev_out) cudaEventDestroy(ev_out);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    void clear_plans() {
+        for (auto& kv : plans) {
+            Plan& p = *kv.second;
+            if (p.graph_layers) cudaGraphExecDestroy(p.graph_layers);
+            if (p.graph_full) cudaGraphExecDestroy(p.graph_full);
+            for (void* q : p.allocs) cudaFree(q);
+            if (p.h_pos) cudaFreeHost(p.h_pos);
+            if (p.h_tok) cudaFreeHost(p.h_tok);
+        }
+        plans.clear();
+    }
+    void free_ws() {
+        for (void* p : ws_allocs) cudaFree(p);
+        ws_allocs.clear();
+        ws_B = 0;
+    }
+
+    // ------------------------------------------------------------ setup --
+    void init(const bd_arch& arch, int dev, int w, int r) {
+        a = arch;
+        device = dev;
+        world = w;
+        rank = r;
+        require(a.vocab >= 1 && a.dim >= 1 && a.n_layers >= 1 && a.n_heads >= 1 &&
+                    a.intermediate >= 1 && a.max_seq >= 1 && a.kv_dim >= 1,
+                BD_ERR_BAD_ARGUMENT, "config: all counts must be >= 1");
+        require(a.dim % a.n_heads == 0, BD_ERR_BAD_ARGUMENT, "config: dim must be divisible by n_heads");
+        hd = a.dim / a.n_heads;
+        require(hd % 2 == 0, BD_ERR_BAD_ARGUMENT, "config: head dimension must be even for rotary embeddings");
+        require(a.kv_dim % hd == 0 && a.dim % a.kv_dim == 0, BD_ERR_BAD_ARGUMENT,
+                "config: kv_dim must be a whole number of heads dividing dim");
+        n_kv_heads = a.kv_dim / hd;
+        require(w >= 1 && r >= 0 && r < w, BD_ERR_BAD_ARGUMENT, "pool: bad world/rank");
+        require(n_kv_heads % w == 0 && a.intermediate % w == 0, BD_ERR_BAD_ARGUMENT,
+                "pool: kv heads and intermediate must divide by world size");
+        require(hd * 2 + a.max_seq <= 48000, BD_ERR_BAD_ARGUMENT, "pool: max_seq too large");
+        q_l = a.dim / w;   q_r0 = q_l * r;
+        kv_l = a.kv_dim / w; kv_r0 = kv_l * r;
+        dim_l = a.dim / w; dim_r0 = dim_l * r;
+        inter_l = a.intermediate / w; inter_r0 = inter_l * r;
+        ld_dim = round_up(a.dim, 8);
+        ld_inter = round_up(a.intermediate, 8);
+        BD_CUDA(cudaSetDevice(device));
+        BD_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        BD_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+        BD_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+        if (const char* e = std::getenv("BD_NO_GRAPH")) use_graphs = (e[0] == '0');
+
+        L.resize(a.n_layers);
+        for (auto& l : L) {
+            l.qkv = dmalloc<uint16_t>((q_l + 2 * kv_l) * ld_dim, &allocs);
+            l.o = dmalloc<uint16_t>(dim_l * ld_dim, &allocs);
+            l.gu = dmalloc<uint16_t>(2 * inter_l * ld_dim, &allocs);
+            l.down = dmalloc<uint16_t>(dim_l * ld_inter, &allocs);
+            BD_CUDA(cudaMemset(l.qkv, 0, (q_l + 2 * kv_l) * ld_dim * 2));
+            BD_CUDA(cudaMemset(l.o, 0, dim_l * ld_dim * 2));
+            BD_CUDA(cudaMemset(l.gu, 0, 2 * inter_l * ld_dim * 2));
+            BD_CUDA(cudaMemset(l.down, 0, dim_l * ld_inter * 2));
+            l.m_qkv = tmap_weights(l.qkv, q_l + 2 * kv_l, a.dim, ld_dim);
+            l.m_o = tmap_weights(l.o, dim_l, a.dim, ld_dim);
+            l.m_gu = tmap_weights(l.gu, 2 * inter_l, a.dim, ld_dim);
+            l.m_down = tmap_weights(l.down, dim_l, a.intermediate, ld_inter);
+        }
+        embed = dmalloc<float>(a.vocab * a.dim, &allocs);
+        lm_head = dmalloc<uint16_t>(a.vocab * ld_dim, &allocs);
+        BD_CUDA(cudaMemset(lm_head, 0, a.vocab * ld_dim * 2));
+        m_lm = tmap_weights(lm_head, a.vocab, a.dim, ld_dim);
+        base_norm1.assign(a.n_layers, std::vector<float>(a.dim, 0.0f));
+        base_norm2.assign(a.n_layers, std::vector<float>(a.dim, 0.0f));
+        base_final_norm.assign(a.dim, 0.0f);
+        have.assign(1 + 9 * a.n_layers + 2, false);
+
+        // RoPE table: the reference's double pow/cos/sin (nn_ops.hpp:33-40), rounded to f32
+        std::vector<float2> tab(a.max_seq * (hd / 2));
+        for (uint64_t p = 0; p < a.max_seq; ++p)
+            for (uint64_t i = 0; i < hd / 2; ++i) {
+                const double freq = std::pow(static_cast<double>(a.rope_theta),
+                                             -2.0 * static_cast<double>(i) / static_cast<double>(hd));
+                const double ang = static_cast<double>(p) * freq;
+                tab[p * (hd / 2) + i] = make_float2(static_cast<float>(std::cos(ang)),
+                                                    static_cast<float>(std::sin(ang)));
+            }
+        rope = dmalloc<float2>(tab.size(), &allocs);
+        BD_CUDA(cudaMemcpy(rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+        backbone_bytes = 0;
+        for (size_t i = 0; i < have.size(); ++i) {
+            uint64_t rr, cc;
+            shape(i, rr, cc);
+            backbone_bytes += 4ull * rr * cc;  // reference accounting: f32 residency (serve.cpp:361)
+        }
+    }
+
+    // tensor_shapes order (P:src/arch.cpp:51-69), kv_dim for k/v (arch.cpp:98-99)
+    void shape(size_t i, uint64_t& rows, uint64_t& cols) const {
+        const size_t last = 1 + 9 * a.n_layers;
+        if (i == 0 || i == last + 1) { rows = a.vocab; cols = a.dim; return; }
+        if (i == last) { rows = 1; cols = a.dim; return; }
+        switch ((i - 1) % 9) {
+            case 0: case 3: rows = a.dim; cols = a.dim; return;
+            case 1: case 2: rows = a.kv_dim; cols = a.dim; return;
+            case 4: case 5: rows = a.intermediate; cols = a.dim; return;
+            case 6: rows = a.dim; cols = a.intermediate; return;
+            default: rows = 1; cols = a.dim; return;
+        }
+    }
+    std::string tname(size_t i) const {
+        const size_t last = 1 + 9 * a.n_layers;
+        if (i == 0) return "embed";
+        if (i == last) return "final_norm";
+        if (i == last + 1) return "lm_head";
+        static const char* roles[9] = {"attn_q", "attn_k", "attn_v", "attn_o", "mlp_gate",
+                                       "mlp_up", "mlp_down", "norm1", "norm2"};
+        return "layers." + std::to_string((i - 1) / 9) + "." + roles[(i - 1) % 9];
+    }
+    int tindex(const std::string& name) const {
+        for (size_t i = 0; i < have.size(); ++i)
+            if (tname(i) == name) return int(i);
+        return -1;
+    }
+
+    // rank-local row range of a projection within its (unsharded) matrix, and
+    // its destination (buffer, row offset in the stacked buffer, ld)
+    void local_rows(int proj, uint64_t& r0, uint64_t& nr) const {
+        switch (proj) {
+            case P_Q: r0 = q_r0; nr = q_l; return;
+            case P_K: case P_V: r0 = kv_r0; nr = kv_l; return;
+            case P_O: case P_DOWN: r0 = dim_r0; nr = dim_l; return;
+            default: r0 = inter_r0; nr = inter_l; return;
+        }
+    }
+    uint64_t stack_offset(int proj) const {
+        switch (proj) {
+            case P_K: return q_l;
+            case P_V: return q_l + kv_l;
+            case P_UP: return inter_l;
+            default: return 0;
+        }
+    }
+
+    void upload_bf16(uint16_t* dst, uint64_t ldd, const void* src, bd_dtype dt, bool is_dev,
+                     uint64_t rows, uint64_t cols, uint64_t src_row0) {
+        const size_t es = dt == BD_BF16 ? 2 : 4;
+        const char* s = static_cast<const char*>(src) + src_row0 * cols * es;
+        if (dt == BD_BF16) {
+            BD_CUDA(cudaMemcpy2D(dst, ldd * 2, s, cols * 2, cols * 2, rows,
+                                 is_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+            return;
+        }
+        const float* dsrc = reinterpret_cast<const float*>(s);
+        float* tmp = nullptr;
+        if (!is_dev) {
+            tmp = dmalloc<float>(rows * cols);
+            BD_CUDA(cudaMemcpy(tmp, s, rows * cols * 4, cudaMemcpyHostToDevice));
+            dsrc = tmp;
+        }
+        f32_to_bf16_2d<<<std::min<uint64_t>((rows * cols + 255) / 256, 4096), 256>>>(
+            dsrc, rows, cols, cols, dst, ldd);
+        note_launch();
+        BD_CUDA(cudaGetLastError());
+        BD_CUDA(cudaDeviceSynchronize());
+        if (tmp) cudaFree(tmp);
+    }
+
+    std::vector<float> to_host_f32(const void* src, bd_dtype dt, bool is_dev, uint64_t n) {
+        std::vector<float> out(n);
+        if (dt == BD_F32) {
+            BD_CUDA(cudaMemcpy(out.data(), src, n * 4, is_dev ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+        } else {
+            std::vector<uint16_t> h(n);
+            BD_CUDA(cudaMemcpy(h.data(), src, n * 2, is_dev ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+            for (uint64_t i = 0; i < n; ++i) {
+                const uint32_t u = uint32_t(h[i]) << 16;
+                std::memcpy(&out[i], &u, 4);
+            }
+        }
+        return out;
+    }
+
+    void set_tensor(const std::string& name, const void* data, bd_dtype dt, bool is_dev,
+                    uint64_t rows, uint64_t cols) {
+        require(dt == BD_F32 || dt == BD_BF16, BD_ERR_UNSUPPORTED_DTYPE,
+                "tensor '" + name + "': unsupported dtype");
+        const int idx = tindex(name);
+        require(idx >= 0, BD_ERR_NAME_MISMATCH, "backbone: unknown tensor '" + name + "'");
+        uint64_t er, ec;
+        shape(idx, er, ec);
+        require(rows == er && cols == ec, BD_ERR_SHAPE_MISMATCH,
+                "backbone: tensor '" + name + "' has shape " + std::to_string(rows) + "x" +
+                    std::to_string(cols) + ", config expects " + std::to_string(er) + "x" +
+                    std::to_string(ec));
+        BD_CUDA(cudaSetDevice(device));
+        const size_t last = 1 + 9 * a.n_layers;
+        if (idx == 0) {
+            const std::vector<float> h = to_host_f32(data, dt, is_dev, rows * cols);
+            BD_CUDA(cudaMemcpy(embed, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+        } else if (size_t(idx) == last) {
+            base_final_norm = to_host_f32(data, dt, is_dev, cols);
+        } else if (size_t(idx) == last + 1) {
+            upload_bf16(lm_head, ld_dim, data, dt, is_dev, rows, cols, 0);
+        } else {
+            const int l = (idx - 1) / 9, role = (idx - 1) % 9;
+            if (role == 7) base_norm1[l] = to_host_f32(data, dt, is_dev, cols);
+            else if (role == 8) base_norm2[l] = to_host_f32(data, dt, is_dev, cols);
+            else {
+                uint64_t r0, nr;
+                local_rows(role, r0, nr);
+                uint16_t* buf;
+                uint64_t ld;
+                switch (role) {
+                    case P_Q: case P_K: case P_V: buf = L[l].qkv; ld = ld_dim; break;
+                    case P_O: buf = L[l].o; ld = ld_dim; break;
+                    case P_GATE: case P_UP: buf = L[l].gu; ld = ld_dim; break;
+                    default: buf = L[l].down; ld = ld_inter; break;
+                }
+                upload_bf16(buf + stack_offset(role) * ld, ld, data, dt, is_dev, nr, cols, r0);
+            }
+        }
+        have[idx] = true;
+    }
+
+    // ---------------------------------------------------------- tenants --
+    struct EntryView {
+        bool packed;
+        uint64_t rows, cols, planes;
+        const uint8_t* bits;
+        const float* scales;
+        const float* raw;
+        bool is_dev;
+    };
+
+    void check_complete() {
+        for (size_t i = 0; i < have.size(); ++i)
+            require(have[i], BD_ERR_NAME_MISMATCH, "backbone: tensor '" + tname(i) + "' not set");
+    }
+
+    // validate coverage & shapes like register_delta (serve.cpp:134-149)
+    std::vector<EntryView> resolve(const std::string& id, const std::map<std::string, EntryView>& ents) {
+        std::vector<EntryView> out;
+        for (size_t i = 0; i < have.size(); ++i) {
+            const std::string n = tname(i);
+            auto it = ents.find(n);
+            require(it != ents.end(), BD_ERR_NAME_MISMATCH,
+                    "delta '" + id + "': missing tensor '" + n + "'");
+            uint64_t er, ec;
+            shape(i, er, ec);
+            require(it->second.rows == er && it->second.cols == ec, BD_ERR_SHAPE_MISMATCH,
+                    "delta '" + id + "': tensor '" + n + "' has shape " +
+                        std::to_string(it->second.rows) + "x" + std::to_string(it->second.cols) +
+                        ", backbone expects " + std::to_string(er) + "x" + std::to_string(ec));
+            out.push_back(it->second);
+        }
+        return out;
+    }
+
+    // host copy of row r of the reconstructed delta (add_delta_row, serve.cpp:39-48)
+    std::vector<float> delta_row(const EntryView& e, uint64_t r) {
+        std::vector<float> row(e.cols, 0.0f);
+        if (e.packed) {
+            const uint64_t nb = (e.rows * e.cols + 7) / 8;
+            for (uint64_t k = 0; k < e.planes; ++k) {
+                // fetch the bytes covering row r
+                const uint64_t b0 = (r * e.cols) >> 3, b1 = ((r + 1) * e.cols + 7) >> 3;
+                std::vector<uint8_t> bytes(b1 - b0);
+                BD_CUDA(cudaMemcpy(bytes.data(), e.bits + k * nb + b0, b1 - b0,
+                                   e.is_dev ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+                for (uint64_t c = 0; c < e.cols; ++c) {
+                    const uint64_t idx = r * e.cols + c - b0 * 8;
+                    row[c] += ((bytes[idx >> 3] >> (idx & 7)) & 1u) ? e.scales[k] : -e.scales[k];
+                }
+            }
+        } else if (e.raw) {  // raw == null encodes an all-zero raw delta
+            BD_CUDA(cudaMemcpy(row.data(), e.raw + r * e.cols, e.cols * 4,
+                               e.is_dev ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+        }
+        return row;
+    }
+
+    float* upload_f32(Tenant& t, const std::vector<float>& v) {
+        float* d = dmalloc<float>(v.size(), &t.allocs);
+        BD_CUDA(cudaMemcpy(d, v.data(), v.size() * 4, cudaMemcpyHostToDevice));
+        return d;
+    }
+
+    std::vector<Plane> upload_planes(Tenant& t, const EntryView& e, uint64_t r0, uint64_t nr) {
+        std::vector<Plane> out;
+        const uint64_t nb = (e.rows * e.cols + 7) / 8;
+        require((r0 * e.cols) % 8 == 0 || nr == e.rows, BD_ERR_BAD_ARGUMENT,
+                "row shard does not start on a byte of the packed plane");
+        const uint64_t b0 = (r0 * e.cols) / 8;
+        const uint64_t len = nr == e.rows ? nb : (nr * e.cols + 7) / 8;
+        for (uint64_t k = 0; k < e.planes; ++k) {
+            uint8_t* d = dmalloc<uint8_t>(round_up(len, 16), &t.allocs);
+            BD_CUDA(cudaMemset(d, 0, round_up(len, 16)));
+            BD_CUDA(cudaMemcpy(d, e.bits + k * nb + b0, len,
+                               e.is_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+            out.push_back({d, e.scales[k]});
+        }
+        return out;
+    }
+
+    float* upload_raw(Tenant& t, const EntryView& e) {
+        if (!e.raw) return nullptr;  // all-zero raw delta: nothing resident
+        float* d = dmalloc<float>(e.rows * e.cols, &t.allocs);
+        BD_CUDA(cudaMemcpy(d, e.raw, e.rows * e.cols * 4,
+                           e.is_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+        return d;
+    }
+
+    void load_tenant(Tenant& t, const std::vector<EntryView>& ev) {
+        BD_CUDA(cudaSetDevice(device));
+        t.proj.assign(a.n_layers, {});
+        t.norm1.assign(a.n_layers, nullptr);
+        t.norm2.assign(a.n_layers, nullptr);
+        t.bytes = 0;
+        for (const auto& e : ev)
+            t.bytes += e.packed ? e.planes * ((e.rows * e.cols + 7) / 8 + 4) : 4ull * e.rows * e.cols;
+        const size_t last = 1 + 9 * a.n_layers;
+        // embedding delta
+        {
+            const EntryView& e = ev[0];
+            if (e.packed) {
+                std::vector<float> full(e.rows * e.cols);
+                for (uint64_t r = 0; r < e.rows; ++r) {
+                    const auto row = delta_row(e, r);
+                    std::copy(row.begin(), row.end(), full.begin() + r * e.cols);
+                }
+                t.embed_raw = upload_f32(t, full);
+            } else {
+                t.embed_raw = upload_raw(t, e);
+            }
+        }
+        for (uint64_t l = 0; l < a.n_layers; ++l) {
+            for (int p = 0; p < P_COUNT; ++p) {
+                const EntryView& e = ev[1 + 9 * l + p];
+                require(e.packed && e.planes >= 1 && e.planes <= kMaxPlanesPerUnit, BD_ERR_BAD_ARGUMENT,
+                        "delta '" + t.id + "': tensor '" + tname(1 + 9 * l + p) +
+                            "' must be packed with 1-4 planes for the device engine");
+                uint64_t r0, nr;
+                local_rows(p, r0, nr);
+                t.proj[l][p] = upload_planes(t, e, r0, nr);
+            }
+            std::vector<float> n1 = base_norm1[l], n2 = base_norm2[l];
+            const auto d1 = delta_row(ev[1 + 9 * l + 7], 0), d2 = delta_row(ev[1 + 9 * l + 8], 0);
+            for (uint64_t i = 0; i < a.dim; ++i) { n1[i] += d1[i]; n2[i] += d2[i]; }
+            t.norm1[l] = upload_f32(t, n1);
+            t.norm2[l] = upload_f32(t, n2);
+        }
+        {
+            std::vector<float> fn = base_final_norm;
+            const auto d = delta_row(ev[last], 0);
+            for (uint64_t i = 0; i < a.dim; ++i) fn[i] += d[i];
+            t.final_norm = upload_f32(t, fn);
+        }
+        {
+            const EntryView& e = ev[last + 1];
+            if (e.packed) {
+                require(e.planes <= kMaxPlanesPerUnit, BD_ERR_BAD_ARGUMENT, "lm_head: too many planes");
+                t.lm_planes = upload_planes(t, e, 0, e.rows);
+            } else {
+                t.lm_raw = upload_raw(t, e);
+            }
+        }
+        t.loaded = true;
+        t.resident = true;
+    }
+
+    void register_entries(const std::string& id, const bd_delta_entry* ents, int n) {
+        require(tenant_idx.count(id) == 0, BD_ERR_DUPLICATE_ID, "delta id already registered: " + id);
+        check_complete();
+        std::map<std::string, EntryView> m;
+        for (int i = 0; i < n; ++i) {
+            const bd_delta_entry& e = ents[i];
+            require(e.name != nullptr, BD_ERR_BAD_ARGUMENT, "delta entry without a name");
+            m[e.name] = EntryView{e.kind == 1, e.rows, e.cols, e.planes, e.bits, e.scales, e.raw,
+                                  e.is_device != 0};
+        }
+        const auto ev = resolve(id, m);
+        Tenant t;
+        t.id = id;
+        load_tenant(t, ev);
+        tenant_idx[id] = int(tenants.size());
+        tenants.push_back(std::move(t));
+    }
+
+    static std::map<std::string, EntryView> views(const DeltaFileHost& f) {
+        std::map<std::string, EntryView> m;
+        for (const auto& e : f.entries)
+            m[e.name] = EntryView{e.packed, e.rows, e.cols, e.planes, e.bits.data(),
+                                  e.scales.data(), e.raw.data(), false};
+        return m;
+    }
+
+    void register_file(const std::string& id, const std::string& path, bool resident) {
+        require(tenant_idx.count(id) == 0, BD_ERR_DUPLICATE_ID, "delta id already registered: " + id);
+        check_complete();
+        const DeltaFileHost f = read_bdelta(path);  // validate even when cold (serve.cpp:132)
+        const auto ev = resolve(id, views(f));
+        Tenant t;
+        t.id = id;
+        t.path = path;
+        if (resident) load_tenant(t, ev);
+        tenant_idx[id] = int(tenants.size());
+        tenants.push_back(std::move(t));
+    }
+
+    // delta_for (serve.cpp:154-166): cold tenants are hot-swapped in on first use
+    void ensure_loaded(int ti) {
+        Tenant& t = tenants[ti];
+        if (t.loaded) return;
+        const auto t0 = std::chrono::steady_clock::now();
+        const DeltaFileHost f = read_bdelta(t.path);
+        load_tenant(t, resolve(t.id, views(f)));
+        BD_CUDA(cudaDeviceSynchronize());
+        const auto t1 = std::chrono::steady_clock::now();
+        stats.cold_loads += 1;
+        stats.last_cold_load_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        clear_plans();
+    }
+
+    uint64_t open_request(const std::string& id) {
+        auto it = tenant_idx.find(id);
+        require(it != tenant_idx.end(), BD_ERR_UNKNOWN_ID, "unknown delta id: " + id);
+        Request r;
+        r.tenant = it->second;
+        r.open = true;
+        const size_t n = a.n_layers * a.max_seq * kv_l;
+        r.kc = dmalloc<uint16_t>(n);
+        r.vc = dmalloc<uint16_t>(n);
+        requests.push_back(r);
+        return requests.size() - 1;
+    }
+
+    void close_request(uint64_t rid) {
+        require(rid < requests.size() && requests[rid].open, BD_ERR_UNKNOWN_ID, "close_request: unknown request");
+        Request& r = requests[rid];
+        r.open = false;
+        cudaFree(r.kc);
+        cudaFree(r.vc);
+        r.kc = r.vc = nullptr;
+        clear_plans();
+    }
+
+    // ------------------------------------------------------------ decode --
+    void ensure_ws(int B) {
+        if (B <= ws_B) return;
+        BD_CUDA(cudaStreamSynchronize(stream));
+        clear_plans();
+        free_ws();
+        ws_B = std::max(B, 16);
+        const uint64_t Mmax = std::max<uint64_t>({q_l + 2 * kv_l, a.dim, 2 * inter_l, a.vocab});
+        x = dmalloc<float>(ws_B * a.dim, &ws_allocs);
+        xn_f32 = dmalloc<float>(ws_B * a.dim, &ws_allocs);
+        xn = dmalloc<uint16_t>(ws_B * ld_dim, &ws_allocs);
+        ctx = dmalloc<uint16_t>(ws_B * ld_dim, &ws_allocs);
+        act = dmalloc<uint16_t>(ws_B * ld_inter, &ws_allocs);
+        BD_CUDA(cudaMemset(xn, 0, ws_B * ld_dim * 2));
+        BD_CUDA(cudaMemset(ctx, 0, ws_B * ld_dim * 2));
+        BD_CUDA(cudaMemset(act, 0, ws_B * ld_inter * 2));
+        D_elems = ws_B * Mmax;
+        D = dmalloc<float>(D_elems, &ws_allocs);
+        // split-K partials: bound by the planner's worst case (<= 32 splits)
+        P_elems = 33ull * ws_B * Mmax;
+        P = dmalloc<float>(P_elems, &ws_allocs);
+        logits = dmalloc<float>(ws_B * a.vocab, &ws_allocs);
+    }
+
+    Plan& plan_for(const std::vector<int>& reqs) {
+        std::string key;
+        for (int r : reqs) key += std::to_string(r) + ",";
+        auto it = plans.find(key);
+        if (it != plans.end()) return *it->second;
+        const int B = int(reqs.size());
+        ensure_ws(B);
+        auto p = std::make_unique<Plan>();
+        p->B = B;
+        p->reqs = reqs;
+        const uint64_t nL = a.n_layers;
+        std::vector<float*> norms((2 * nL + 1) * B);
+        std::vector<uint16_t*> kc(B), vc(B);
+        std::vector<float*> emb(B), lmr(B);
+        bool any_lmraw = false;
+        for (int b = 0; b < B; ++b) {
+            const Request& r = requests[reqs[b]];
+            const Tenant& t = tenants[r.tenant];
+            for (uint64_t l = 0; l < nL; ++l) {
+                norms[(2 * l) * B + b] = t.norm1[l];
+                norms[(2 * l + 1) * B + b] = t.norm2[l];
+            }
+            norms[(2 * nL) * B + b] = t.final_norm;
+            kc[b] = r.kc;
+            vc[b] = r.vc;
+            emb[b] = t.embed_raw;
+            lmr[b] = t.lm_raw;
+            any_lmraw |= t.lm_raw != nullptr;
+        }
+        auto upload_ptrs = [&](auto& vec) {
+            using T = typename std::remove_reference<decltype(vec)>::type::value_type;
+            T* d = dmalloc<T>(vec.size(), &p->allocs);
+            BD_CUDA(cudaMemcpy(d, vec.data(), vec.size() * sizeof(T), cudaMemcpyHostToDevice));
+            return d;
+        };
+        p->d_norm = upload_ptrs(norms);
+        p->d_kc = upload_ptrs(kc);
+        p->d_vc = upload_ptrs(vc);
+        p->d_embed = upload_ptrs(emb);
+        p->d_lmraw = any_lmraw ? upload_ptrs(lmr) : nullptr;
+        p->d_pos = dmalloc<int>(B, &p->allocs);
+        p->d_tok = dmalloc<int>(B, &p->allocs);
+        BD_CUDA(cudaMallocHost(&p->h_pos, B * sizeof(int)));
+        BD_CUDA(cudaMallocHost(&p->h_tok, B * sizeof(int)));
+
+        // tenant segmentation
+        std::vector<int> order;
+        std::map<int, std::vector<int>> by_t;
+        for (int b = 0; b < B; ++b) {
+            const int t = requests[reqs[b]].tenant;
+            if (!by_t.count(t)) order.push_back(t);
+            by_t[t].push_back(b);
+        }
+        auto units_for = [&](std::initializer_list<int> projs, uint64_t l) {
+            std::vector<DeltaUnit> out;
+            for (int t : order) {
+                const auto& rq = by_t[t];
+                for (size_t c = 0; c < rq.size(); c += kMaxReqPerUnit) {
+                    for (int pj : projs) {
+                        DeltaUnit u{};
+                        const auto& planes = tenants[t].proj[l][pj];
+                        u.n_planes = int(planes.size());
+                        for (size_t k = 0; k < planes.size(); ++k) {
+                            u.bits[k] = planes[k].bits;
+                            u.alpha[k] = planes[k].alpha;
+                        }
+                        uint64_t r0, nr;
+                        local_rows(pj, r0, nr);
+                        u.row0 = int(stack_offset(pj));
+                        u.rows = int(nr);
+                        u.n_req = int(std::min<size_t>(kMaxReqPerUnit, rq.size() - c));
+                        for (int q = 0; q < u.n_req; ++q) u.req[q] = rq[c + q];
+                        out.push_back(u);
+                    }
+                }
+            }
+            return out;
+        };
+        p->units.resize(nL);
+        for (uint64_t l = 0; l < nL; ++l) {
+            p->units[l][0] = units_for({P_Q, P_K, P_V}, l);
+            p->units[l][1] = units_for({P_O}, l);
+            p->units[l][2] = units_for({P_GATE, P_UP}, l);
+            p->units[l][3] = units_for({P_DOWN}, l);
+        }
+        for (int t : order) {
+            const auto& rq = by_t[t];
+            const auto& planes = tenants[t].lm_planes;
+            if (planes.empty()) continue;
+            for (size_t c = 0; c < rq.size(); c += kMaxReqPerUnit) {
+                DeltaUnit u{};
+                u.n_planes = int(planes.size());
+                for (size_t k = 0; k < planes.size(); ++k) {
+                    u.bits[k] = planes[k].bits;
+                    u.alpha[k] = planes[k].alpha;
+                }
+                u.row0 = 0;
+                u.rows = int(a.vocab);
+                u.n_req = int(std::min<size_t>(kMaxReqPerUnit, rq.size() - c));
+                for (int q = 0; q < u.n_req; ++q) u.req[q] = rq[c + q];
+                p->lm_units.push_back(u);
+            }
+        }
+        p->g_qkv = plan_base_gemm(q_l + 2 * kv_l, a.dim, B);
+        p->g_o = plan_base_gemm(dim_l, a.dim, B);
+        p->g_gu = plan_base_gemm(2 * inter_l, a.dim, B);
+        p->g_down = plan_base_gemm(dim_l, a.intermediate, B);
+        p->g_lm = plan_base_gemm(a.vocab, a.dim, B);
+        for (const GemmPlan* g : {&p->g_qkv, &p->g_o, &p->g_gu, &p->g_down, &p->g_lm})
+            require(uint64_t(g->splits) * B * g->M <= P_elems, BD_ERR_CUDA, "split-K workspace too small");
+        const int bn = p->g_qkv.bn;
+        p->x_xn = tmap_acts(xn, B, a.dim, ld_dim, bn);
+        p->x_ctx = tmap_acts(ctx, B, a.dim, ld_dim, bn);
+        p->x_act = tmap_acts(act, B, a.intermediate, ld_inter, bn);
+        auto& slot = plans[key];
+        slot = std::move(p);
+        return *slot;
+    }
+
+    ProjOut proj_out(const GemmPlan& g, bool with_delta) const {
+        ProjOut o;
+        o.P = P;
+        o.splits = g.splits;
+        o.pstride = size_t(g.batch) * g.M;
+        o.D = with_delta ? D : nullptr;
+        o.M = int(g.M);
+        return o;
+    }
+
+    void linear(const GemmPlan& g, const CUtensorMap& mw, const CUtensorMap& mx,
+                const std::vector<DeltaUnit>& units, const uint16_t* X, int ldx, int cols, int B,
+                cudaStream_t s) {
+        base_gemm_launch(g, mw, mx, P, s);
+        delta_units_launch(units.data(), int(units.size()), X, ldx, cols, B, D, int(g.M), s);
+    }
+
+    // the layer loop of decode_shared (serve.cpp:240-310); x holds the
+    // residual stream entering layer 0 and leaves it after the last layer
+    void run_layers(Plan& p, cudaStream_t s) {
+        const int B = p.B;
+        const uint64_t nL = a.n_layers;
+        AttnArgs aa{int(a.dim), int(a.kv_dim), int(a.n_heads), int(n_kv_heads), int(hd),
+                    int(a.max_seq), 0, p.d_kc, p.d_vc, rope};
+        ProjOut prev;  // pending residual contribution (previous layer's down)
+        for (uint64_t l = 0; l < nL; ++l) {
+            const LayerW& W = L[l];
+            // x += down(prev); xn = norm1(x)
+            resid_norm_launch(x, B, int(a.dim), prev, p.d_norm + (2 * l) * B, xn, int(ld_dim),
+                              nullptr, s);
+            linear(p.g_qkv, W.m_qkv, p.x_xn, p.units[l][0], xn, int(ld_dim), int(a.dim), B, s);
+            aa.layer = int(l);
+            attn_launch(proj_out(p.g_qkv, true), aa, p.d_pos, B, ctx, int(ld_dim), s);
+            linear(p.g_o, W.m_o, p.x_ctx, p.units[l][1], ctx, int(ld_dim), int(a.dim), B, s);
+            resid_norm_launch(x, B, int(a.dim), proj_out(p.g_o, true), p.d_norm + (2 * l + 1) * B,
+                              xn, int(ld_dim), nullptr, s);
+            linear(p.g_gu, W.m_gu, p.x_xn, p.units[l][2], xn, int(ld_dim), int(a.dim), B, s);
+            silu_launch(proj_out(p.g_gu, true), B, int(a.intermediate), act, int(ld_inter), s);
+            linear(p.g_down, W.m_down, p.x_act, p.units[l][3], act, int(ld_inter),
+                   int(a.intermediate), B, s);
+            prev = proj_out(p.g_down, true);
+        }
+        resid_norm_launch(x, B, int(a.dim), prev, nullptr, nullptr, 0, nullptr, s);
+    }
+
+    void run_full(Plan& p, cudaStream_t s) {
+        const int B = p.B;
+        embed_launch(embed, p.d_tok, p.d_embed, B, int(a.dim), x, s);
+        run_layers(p, s);
+        resid_norm_launch(x, B, int(a.dim), ProjOut{}, p.d_norm + (2 * a.n_layers) * B, xn,
+                          int(ld_dim), xn_f32, s);
+        base_gemm_launch(p.g_lm, m_lm, p.x_xn, P, s);
+        delta_units_launch(p.lm_units.data(), int(p.lm_units.size()), xn, int(ld_dim), int(a.dim),
+                           B, D, int(a.vocab), s);
+        logits_launch(proj_out(p.g_lm, true), p.d_lmraw, xn_f32, B, int(a.dim), int(a.vocab),
+                      logits, s);
+    }
+
+    void execute(Plan& p, bool full) {
+        cudaGraphExec_t& g = full ? p.graph_full : p.graph_layers;
+        uint64_t& kcount = full ? p.kernels_full : p.kernels_layers;
+        if (!use_graphs) {
+            const uint64_t c0 = launch_count();
+            if (full) run_full(p, stream); else run_layers(p, stream);
+            stats.kernels_last_step = launch_count() - c0;
+            return;
+        }
+        if (!g) {
+            cudaGraph_t graph;
+            const uint64_t c0 = launch_count();
+            BD_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+            try {
+                if (full) run_full(p, stream); else run_layers(p, stream);
+            } catch (...) {
+                cudaStreamEndCapture(stream, &graph);
+                throw;
+            }
+            BD_CUDA(cudaStreamEndCapture(stream, &graph));
+            kcount = launch_count() - c0;
+            BD_CUDA(cudaGraphInstantiate(&g, graph, 0));
+            BD_CUDA(cudaGraphDestroy(graph));
+        }
+        BD_CUDA(cudaGraphLaunch(g, stream));
+        stats.kernels_last_step = kcount;
+    }
+
+    void validate(const bd_request* reqs, uint64_t n) {
+        for (uint64_t i = 0; i < n; ++i) {
+            const bd_request& q = reqs[i];
+            require(q.request_id < requests.size() && requests[q.request_id].open, BD_ERR_UNKNOWN_ID,
+                    "decode: unknown request id");
+            const Request& r = requests[q.request_id];
+            require(q.position == r.pos, BD_ERR_BAD_ARGUMENT,
+                    "decode: request position does not match cache position");
+            require(r.pos < a.max_seq, BD_ERR_BAD_ARGUMENT, "decode: context exceeds max_seq");
+            require(q.token >= 0 && uint64_t(q.token) < a.vocab, BD_ERR_BAD_TOKEN,
+                    "decode: token id out of range");
+            for (uint64_t j = 0; j < i; ++j)
+                require(reqs[j].request_id != q.request_id, BD_ERR_BAD_ARGUMENT,
+                        "decode: request appears twice in one batch");
+        }
+    }
+
+    void step(const bd_request* reqs, uint64_t n, bool full, const float* x_in, float* x_out,
+              float* host_logits, cudaStream_t user) {
+        BD_CUDA(cudaSetDevice(device));
+        validate(reqs, n);
+        if (n == 0) return;
+        require(n <= 256, BD_ERR_BAD_ARGUMENT, "decode: batch must be <= 256");
+        std::vector<int> idx(n);
+        for (uint64_t i = 0; i < n; ++i) {
+            idx[i] = int(reqs[i].request_id);
+            ensure_loaded(requests[idx[i]].tenant);
+        }
+        Plan& p = plan_for(idx);
+        // order the pool stream after the caller's stream
+        BD_CUDA(cudaEventRecord(ev_in, user));
+        BD_CUDA(cudaStreamWaitEvent(stream, ev_in, 0));
+        BD_CUDA(cudaStreamSynchronize(stream));  // pinned staging reuse
+        for (uint64_t i = 0; i < n; ++i) {
+            p.h_pos[i] = int(reqs[i].position);
+            p.h_tok[i] = reqs[i].token;
+        }
+        BD_CUDA(cudaMemcpyAsync(p.d_pos, p.h_pos, n * sizeof(int), cudaMemcpyHostToDevice, stream));
+        BD_CUDA(cudaMemcpyAsync(p.d_tok, p.h_tok, n * sizeof(int), cudaMemcpyHostToDevice, stream));
+        if (!full)
+            BD_CUDA(cudaMemcpyAsync(x, x_in, n * a.dim * 4, cudaMemcpyDeviceToDevice, stream));
+        execute(p, full);
+        if (full) {
+            if (host_logits)
+                BD_CUDA(cudaMemcpyAsync(host_logits, logits, n * a.vocab * 4, cudaMemcpyDeviceToHost,
+                                        stream));
+        } else {
+            BD_CUDA(cudaMemcpyAsync(x_out, x, n * a.dim * 4, cudaMemcpyDeviceToDevice, stream));
+        }
+        BD_CUDA(cudaEventRecord(ev_out, stream));
+        BD_CUDA(cudaStreamWaitEvent(user, ev_out, 0));
+        if (full && host_logits) BD_CUDA(cudaStreamSynchronize(stream));
+        for (uint64_t i = 0; i < n; ++i) requests[idx[i]].pos += 1;
+    }
+
+    void decode(const bd_request* reqs, uint64_t n, int mode, float* logits_host, cudaStream_t user) {
+        require(mode == 0 || mode == 1, BD_ERR_BAD_ARGUMENT, "decode: mode must be 0 (shared) or 1 (naive)");
+        if (mode == 0) {
+            validate(reqs, n);
+            stats.backbone_passes += 1;  // serve.cpp:210
+            step(reqs, n, true, nullptr, nullptr, logits_host, user);
+        } else {
+            // naive (serve.cpp:327-342): one backbone pass per request
+            validate(reqs, n);
+            stats.backbone_passes += n;
+            for (uint64_t i = 0; i < n; ++i)
+                step(reqs + i, 1, true, nullptr, nullptr, logits_host ? logits_host + i * a.vocab : nullptr,
+                     user);
+        }
+    }
+
+    uint64_t resident_bytes() const {
+        uint64_t tot = backbone_bytes;
+        for (const auto& t : tenants)
+            if (t.loaded) tot += t.bytes;
+        for (const auto& r : requests)
+            if (r.open) tot += 2ull * 4ull * r.pos * a.kv_dim * a.n_layers;  // KvCache::bytes (f32 accounting)
+        return tot;
+    }
+};
+
+}  // namespace bd
+
+struct bd_pool {
+    bd::PoolImpl impl;
+};
+
+namespace bd {
+bd_pool* pool_create(const bd_arch& a, int device, int world, int rank) {
+    auto* p = new bd_pool;
+    try {
+        p->impl.init(a, device, world, rank);
+    } catch (...) {
+        delete p;
+        throw;
+    }
+    return p;
+}
+void pool_destroy(bd_pool* p) { delete p; }
+void pool_set_tensor(bd_pool* p, const char* name, const void* data, bd_dtype dt, int is_dev,
+                     uint64_t rows, uint64_t cols) {
+    require(name && data, BD_ERR_BAD_ARGUMENT, "set_tensor: null argument");
+    p->impl.set_tensor(name, data, dt, is_dev != 0, rows, cols);
+}
+void pool_register(bd_pool* p, const char* id, const bd_delta_entry* e, int n) {
+    require(id && (e || n == 0), BD_ERR_BAD_ARGUMENT, "register_delta: null argument");
+    p->impl.register_entries(id, e, n);
+}
+void pool_register_file(bd_pool* p, const char* id, const char* path, int resident) {
+    require(id && path, BD_ERR_BAD_ARGUMENT, "register_delta_file: null argument");
+    p->impl.register_file(id, path, resident != 0);
+}
+uint64_t pool_open(bd_pool* p, const char* id) {
+    require(id != nullptr, BD_ERR_BAD_ARGUMENT, "open_request: null id");
+    return p->impl.open_request(id);
+}
+void pool_close(bd_pool* p, uint64_t rid) { p->impl.close_request(rid); }
+void pool_decode(bd_pool* p, const bd_request* r, uint64_t n, int mode, float* logits, void* s) {
+    require(r || n == 0, BD_ERR_BAD_ARGUMENT, "decode: null requests");
+    p->impl.decode(r, n, mode, logits, static_cast<cudaStream_t>(s));
+}
+void pool_decode_layers(bd_pool* p, const bd_request* r, uint64_t n, const float* xin, float* xout,
+                        void* s) {
+    require((r && xin && xout) || n == 0, BD_ERR_BAD_ARGUMENT, "decode_layers: null argument");
+    p->impl.validate(r, n);
+    p->impl.stats.backbone_passes += 1;
+    p->impl.step(r, n, false, xin, xout, nullptr, static_cast<cudaStream_t>(s));
+}
+void pool_stats(const bd_pool* p, bd_pool_stats* out) {
+    *out = p->impl.stats;
+    out->resident_bytes = p->impl.resident_bytes();
+}
+}  // namespace bd

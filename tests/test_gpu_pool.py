@@ -1,0 +1,213 @@
+"""GPU ServingPool (bd_pool_*) parity with the reference ServingPool
+(P:tests/test_serve.cpp, acceptance.cpp criterion 3) and the oracle port.
+
+Tolerances: the device pool computes in bf16 (weights, GEMM activations, KV)
+with f32 accumulation, so logits are compared with relative L2 <= 1e-2 against
+the f32 reference (north star's bf16 tolerance), and <= 2e-3 against the port
+run on the same bf16-rounded backbone. Determinism / permutation / counters
+are exact."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2402_10193_b200 as bd
+from conftest import GOLDEN
+from paper_2402_10193_b200 import bdelta
+from paper_2402_10193_b200.serving import ServingPool, tensor_shapes
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_l2(got, want):
+    got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
+    return np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30)
+
+
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(torch.bfloat16).float().numpy()
+
+
+@pytest.fixture(scope="module")
+def toy():
+    d = np.load(os.path.join(GOLDEN, "toy_decode.npz"))
+    cfg = json.loads(str(d["cfg"]))
+    arch = dict(cfg, kv_dim=cfg["dim"])
+    return d, arch
+
+
+def tensors_of(arch, flat):
+    out, off = {}, 0
+    for name, r, c in tensor_shapes(arch):
+        out[name] = flat[off:off + r * c].reshape(r, c)
+        off += r * c
+    return out
+
+
+def make_pool(cuda, arch, base, n_tenants=4, resident=True):
+    pool = ServingPool(arch, tensors_of(arch, base))
+    for i in range(n_tenants):
+        pool.register_delta(f"t{i}", os.path.join(GOLDEN, f"toy_t{i}.bdelta"), resident)
+    return pool
+
+
+def test_shared_matches_reference_logits(cuda, toy):
+    """acceptance.cpp:133-173 / test_serve.cpp:103-132 against the golden reference logits."""
+    d, arch = toy
+    for B in (1, 2, 4):
+        pool = make_pool(cuda, arch, d["base"])
+        rids = [pool.open_request(f"t{i % 4}") for i in range(B)]
+        for pos, tok in enumerate(d[f"B{B}_tokens"]):
+            got = pool.decode_step([(r, int(tok), pos) for r in rids])
+            want = d[f"B{B}_logits"][pos]
+            for i in range(B):
+                assert rel_l2(got[i], want[i]) <= 1e-2, (B, pos, i, rel_l2(got[i], want[i]))
+        pool.close()
+
+
+def test_shared_matches_port_on_bf16_backbone(cuda, toy, port):
+    d, arch = toy
+    base16 = bf16_round(d["base"])
+    names = [n for n, _, _ in tensor_shapes(arch)]
+    tens = [[bdelta.read(os.path.join(GOLDEN, f"toy_t{i}.bdelta"))[n] for n in names] for i in range(4)]
+    B = 4
+    pool = make_pool(cuda, arch, base16)
+    rids = [pool.open_request(f"t{i}") for i in range(B)]
+    kc = [np.zeros((arch["n_layers"], arch["max_seq"], arch["kv_dim"]), np.float32) for _ in range(B)]
+    vc = [np.zeros_like(k) for k in kc]
+    toks = d["B4_tokens"]
+    for pos, tok in enumerate(toks):
+        got = pool.decode_step([(r, int(tok), pos) for r in rids])
+        want = port.decode(arch, base16, tens, list(range(B)), [int(tok)] * B, [pos] * B, kc, vc)
+        for i in range(B):
+            assert rel_l2(got[i], want[i]) <= 2e-3, (pos, i, rel_l2(got[i], want[i]))
+
+
+def test_identical_contexts_identical_outputs(cuda, toy):
+    """test_serve.cpp:134-145"""
+    d, arch = toy
+    pool = make_pool(cuda, arch, d["base"], 1)
+    a, b = pool.open_request("t0"), pool.open_request("t0")
+    out = pool.decode_step([(a, 7, 0), (b, 7, 0)])
+    assert np.array_equal(out[0], out[1])
+
+
+def test_permutation_bit_identical(cuda, toy):
+    """test_serve.cpp:169-190"""
+    d, arch = toy
+
+    def run(order):
+        pool = make_pool(cuda, arch, d["base"], 3)
+        reqs = [pool.open_request(f"t{i}") for i in range(3)]
+        out = None
+        for pos in range(2):
+            out = pool.decode_step([(reqs[i], 5 + i, pos) for i in order])
+        return out
+
+    fwd, rev = run([0, 1, 2]), run([2, 1, 0])
+    for i in range(3):
+        assert np.array_equal(fwd[i], rev[2 - i])
+
+
+def test_zero_delta_equals_backbone(cuda, toy, port):
+    """test_serve.cpp:147-167: a zero delta decodes like the plain backbone."""
+    d, arch = toy
+    base16 = bf16_round(d["base"])
+    pool = ServingPool(arch, tensors_of(arch, base16))
+    pool.register_delta("zero", os.path.join(GOLDEN, "toy_zero.bdelta"))
+    r = pool.open_request("zero")
+    names = [n for n, _, _ in tensor_shapes(arch)]
+    zero = [bdelta.read(os.path.join(GOLDEN, "toy_zero.bdelta"))[n] for n in names]
+    kc = [np.zeros((arch["n_layers"], arch["max_seq"], arch["kv_dim"]), np.float32)]
+    vc = [np.zeros_like(kc[0])]
+    for pos, tok in enumerate([3, 11, 40, 2, 9]):
+        got = pool.decode_step([(r, tok, pos)])[0]
+        want = port.decode(arch, base16, [zero], [0], [tok], [pos], kc, vc)[0]
+        assert rel_l2(got, want) <= 2e-3
+
+
+def test_backbone_pass_counter(cuda, toy):
+    """test_serve.cpp:192-210"""
+    d, arch = toy
+    pool = make_pool(cuda, arch, d["base"])
+    reqs = [pool.open_request(f"t{i}") for i in range(4)]
+    pool.decode_step([(r, 1, 0) for r in reqs])
+    assert pool.stats()["backbone_passes"] == 1
+    pool.decode_step([(r, 1, 1) for r in reqs])
+    assert pool.stats()["backbone_passes"] == 2
+    pool.decode_step([(r, 1, 2) for r in reqs], mode="naive")
+    assert pool.stats()["backbone_passes"] == 2 + 4
+
+
+def test_naive_matches_shared(cuda, toy):
+    d, arch = toy
+    ps, pn = make_pool(cuda, arch, d["base"]), make_pool(cuda, arch, d["base"])
+    rs = [ps.open_request(f"t{i}") for i in range(4)]
+    rn = [pn.open_request(f"t{i}") for i in range(4)]
+    for pos, tok in enumerate([1, 2, 3]):
+        zs = ps.decode_step([(r, tok, pos) for r in rs])
+        zn = pn.decode_step([(r, tok, pos) for r in rn], mode="naive")
+        for i in range(4):
+            assert rel_l2(zs[i], zn[i]) <= 1e-4
+
+
+def test_cold_registration_hot_swap(cuda, toy):
+    """test_serve.cpp:62-76"""
+    d, arch = toy
+    pool = ServingPool(arch, tensors_of(arch, d["base"]))
+    before = pool.resident_bytes()
+    pool.register_delta("cold", os.path.join(GOLDEN, "toy_t0.bdelta"), resident=False)
+    assert pool.resident_bytes() == before and pool.stats()["cold_loads"] == 0
+    r = pool.open_request("cold")
+    pool.decode_step([(r, 3, 0)])
+    st = pool.stats()
+    assert st["cold_loads"] == 1 and st["last_cold_load_ms"] > 0
+    assert pool.resident_bytes() > before
+
+
+def test_registration_and_decode_errors(cuda, toy, tmp_path):
+    d, arch = toy
+    pool = make_pool(cuda, arch, d["base"], 1)
+    with pytest.raises(bd.BitDeltaError) as e:
+        pool.register_delta("t0", os.path.join(GOLDEN, "toy_t0.bdelta"))
+    assert e.value.code == "duplicate_id"
+    # wrong-arch delta names the first offending tensor (test_serve.cpp:78-100)
+    f = bdelta.read(os.path.join(GOLDEN, "toy_t0.bdelta"))
+    f["embed"] = {"kind": "raw", "rows": 2, "cols": 2, "raw": np.zeros((2, 2), np.float32)}
+    p = str(tmp_path / "bad.bdelta")
+    bdelta.write(f, p)
+    with pytest.raises(bd.BitDeltaError) as e:
+        pool.register_delta("bad", p)
+    assert e.value.code == "shape_mismatch" and "'embed'" in str(e.value)
+    r = pool.open_request("t0")
+    with pytest.raises(bd.BitDeltaError) as e:
+        pool.decode_step([(r, 10_000, 0)])
+    assert e.value.code == "bad_token"
+    with pytest.raises(bd.BitDeltaError) as e:
+        pool.decode_step([(r, 1, 3)])
+    assert e.value.code == "bad_argument"
+    with pytest.raises(bd.BitDeltaError) as e:
+        pool.decode_step([(99, 1, 0)])
+    assert e.value.code == "unknown_id"
+    with pytest.raises(bd.BitDeltaError) as e:
+        pool.open_request("nope")
+    assert e.value.code == "unknown_id"
+
+
+def test_memory_accounting(cuda, toy):
+    """test_serve.cpp:212-241: resident = backbone + delta payloads + caches."""
+    d, arch = toy
+    pool = make_pool(cuda, arch, d["base"], 2)
+    backbone = sum(4 * r * c for _, r, c in tensor_shapes(arch))
+    payload = 0
+    for i in range(2):
+        for e in bdelta.read(os.path.join(GOLDEN, f"toy_t{i}.bdelta")).values():
+            payload += e["planes"] * (e["bits"].shape[1] + 4) if e["kind"] == "packed" else 4 * e["raw"].size
+    assert pool.resident_bytes() == backbone + payload
+    r0, r1 = pool.open_request("t0"), pool.open_request("t1")
+    for pos in range(3):
+        pool.decode_step([(r0, 1, pos), (r1, 2, pos)])
+    kv = 2 * 2 * 4 * 3 * arch["dim"] * arch["n_layers"]
+    assert pool.resident_bytes() == backbone + payload + kv
