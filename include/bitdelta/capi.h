@@ -178,6 +178,18 @@ int bd_pool_decode_step(bd_pool* pool, const bd_request* reqs, uint64_t n, int m
 int bd_pool_decode_layers(bd_pool* pool, const bd_request* reqs, uint64_t n, const float* x_in,
                           float* x_out, void* stream);
 
+/* Profiled layer step: same work as bd_pool_decode_layers (advances positions),
+ * run eagerly (no graph) with CUDA events on the launching stream around every
+ * kernel; ms_out[k] / count_out[k] receive total device ms and launches per
+ * kind k (bd_prof_kind). Used by bench.py for the per-kernel roofline. */
+enum bd_prof_kind {
+    BD_PROF_GEMM_QKV = 0, BD_PROF_GEMM_O, BD_PROF_GEMM_GU, BD_PROF_GEMM_DOWN,
+    BD_PROF_DELTA_QKV, BD_PROF_DELTA_O, BD_PROF_DELTA_GU, BD_PROF_DELTA_DOWN,
+    BD_PROF_ATTN, BD_PROF_NORM, BD_PROF_SILU, BD_PROF_KINDS
+};
+int bd_pool_profile_layers(bd_pool* pool, const bd_request* reqs, uint64_t n, const float* x_in,
+                           float* x_out, double* ms_out, uint64_t* count_out, void* stream);
+
 typedef struct bd_pool_stats {
     uint64_t backbone_passes; /* serve.hpp:77 */
     uint64_t cold_loads;      /* serve.hpp:78 */

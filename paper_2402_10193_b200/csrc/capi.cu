@@ -40,6 +40,8 @@ void pool_decode(bd_pool* p, const bd_request* r, uint64_t n, int mode, float* l
 void pool_decode_layers(bd_pool* p, const bd_request* r, uint64_t n, const float* xin, float* xout,
                         void* s);
 void pool_stats(const bd_pool* p, bd_pool_stats* out);
+void pool_profile_layers(bd_pool* p, const bd_request* r, uint64_t n, const float* xin,
+                         float* xout, double* ms, uint64_t* cnt, void* s);
 
 template <class F>
 int guarded(F&& f) {
@@ -244,6 +246,13 @@ int bd_pool_decode_layers(bd_pool* pool, const bd_request* reqs, uint64_t n, con
     return guarded([&] {
         require(pool != nullptr, BD_ERR_BAD_ARGUMENT, "null pool");
         pool_decode_layers(pool, reqs, n, x_in, x_out, stream);
+    });
+}
+int bd_pool_profile_layers(bd_pool* pool, const bd_request* reqs, uint64_t n, const float* x_in,
+                           float* x_out, double* ms_out, uint64_t* count_out, void* stream) {
+    return guarded([&] {
+        require(pool != nullptr, BD_ERR_BAD_ARGUMENT, "null pool");
+        pool_profile_layers(pool, reqs, n, x_in, x_out, ms_out, count_out, stream);
     });
 }
 int bd_pool_get_stats(const bd_pool* pool, bd_pool_stats* out) {

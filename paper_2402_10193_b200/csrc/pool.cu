@@ -762,11 +762,31 @@ struct PoolImpl {
         return o;
     }
 
-    void linear(const GemmPlan& g, const CUtensorMap& mw, const CUtensorMap& mx,
+    // ---- optional per-kernel profiling (eager mode only) ----
+    bool profiling = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_events;
+    template <class F>
+    void prof(int kind, cudaStream_t s, F&& f) {
+        if (!profiling) {
+            f();
+            return;
+        }
+        cudaEvent_t e0, e1;
+        BD_CUDA(cudaEventCreate(&e0));
+        BD_CUDA(cudaEventCreate(&e1));
+        BD_CUDA(cudaEventRecord(e0, s));
+        f();
+        BD_CUDA(cudaEventRecord(e1, s));
+        prof_events.push_back({kind, {e0, e1}});
+    }
+
+    void linear(int group, const GemmPlan& g, const CUtensorMap& mw, const CUtensorMap& mx,
                 const std::vector<DeltaUnit>& units, const uint16_t* X, int ldx, int cols, int B,
                 cudaStream_t s) {
-        base_gemm_launch(g, mw, mx, P, s);
-        delta_units_launch(units.data(), int(units.size()), X, ldx, cols, B, D, int(g.M), s);
+        prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm_launch(g, mw, mx, P, s); });
+        prof(BD_PROF_DELTA_QKV + group, s, [&] {
+            delta_units_launch(units.data(), int(units.size()), X, ldx, cols, B, D, int(g.M), s);
+        });
     }
 
     // the layer loop of decode_shared (serve.cpp:240-310); x holds the
@@ -780,21 +800,31 @@ struct PoolImpl {
         for (uint64_t l = 0; l < nL; ++l) {
             const LayerW& W = L[l];
             // x += down(prev); xn = norm1(x)
-            resid_norm_launch(x, B, int(a.dim), prev, p.d_norm + (2 * l) * B, xn, int(ld_dim),
-                              nullptr, s);
-            linear(p.g_qkv, W.m_qkv, p.x_xn, p.units[l][0], xn, int(ld_dim), int(a.dim), B, s);
+            prof(BD_PROF_NORM, s, [&] {
+                resid_norm_launch(x, B, int(a.dim), prev, p.d_norm + (2 * l) * B, xn, int(ld_dim),
+                                  nullptr, s);
+            });
+            linear(0, p.g_qkv, W.m_qkv, p.x_xn, p.units[l][0], xn, int(ld_dim), int(a.dim), B, s);
             aa.layer = int(l);
-            attn_launch(proj_out(p.g_qkv, true), aa, p.d_pos, B, ctx, int(ld_dim), s);
-            linear(p.g_o, W.m_o, p.x_ctx, p.units[l][1], ctx, int(ld_dim), int(a.dim), B, s);
-            resid_norm_launch(x, B, int(a.dim), proj_out(p.g_o, true), p.d_norm + (2 * l + 1) * B,
-                              xn, int(ld_dim), nullptr, s);
-            linear(p.g_gu, W.m_gu, p.x_xn, p.units[l][2], xn, int(ld_dim), int(a.dim), B, s);
-            silu_launch(proj_out(p.g_gu, true), B, int(a.intermediate), act, int(ld_inter), s);
-            linear(p.g_down, W.m_down, p.x_act, p.units[l][3], act, int(ld_inter),
+            prof(BD_PROF_ATTN, s, [&] {
+                attn_launch(proj_out(p.g_qkv, true), aa, p.d_pos, B, ctx, int(ld_dim), s);
+            });
+            linear(1, p.g_o, W.m_o, p.x_ctx, p.units[l][1], ctx, int(ld_dim), int(a.dim), B, s);
+            prof(BD_PROF_NORM, s, [&] {
+                resid_norm_launch(x, B, int(a.dim), proj_out(p.g_o, true),
+                                  p.d_norm + (2 * l + 1) * B, xn, int(ld_dim), nullptr, s);
+            });
+            linear(2, p.g_gu, W.m_gu, p.x_xn, p.units[l][2], xn, int(ld_dim), int(a.dim), B, s);
+            prof(BD_PROF_SILU, s, [&] {
+                silu_launch(proj_out(p.g_gu, true), B, int(a.intermediate), act, int(ld_inter), s);
+            });
+            linear(3, p.g_down, W.m_down, p.x_act, p.units[l][3], act, int(ld_inter),
                    int(a.intermediate), B, s);
             prev = proj_out(p.g_down, true);
         }
-        resid_norm_launch(x, B, int(a.dim), prev, nullptr, nullptr, 0, nullptr, s);
+        prof(BD_PROF_NORM, s, [&] {
+            resid_norm_launch(x, B, int(a.dim), prev, nullptr, nullptr, 0, nullptr, s);
+        });
     }
 
     void run_full(Plan& p, cudaStream_t s) {
@@ -813,7 +843,7 @@ struct PoolImpl {
     void execute(Plan& p, bool full) {
         cudaGraphExec_t& g = full ? p.graph_full : p.graph_layers;
         uint64_t& kcount = full ? p.kernels_full : p.kernels_layers;
-        if (!use_graphs) {
+        if (!use_graphs || profiling) {
             const uint64_t c0 = launch_count();
             if (full) run_full(p, stream); else run_layers(p, stream);
             stats.kernels_last_step = launch_count() - c0;
@@ -965,6 +995,37 @@ void pool_decode_layers(bd_pool* p, const bd_request* r, uint64_t n, const float
     p->impl.validate(r, n);
     p->impl.stats.backbone_passes += 1;
     p->impl.step(r, n, false, xin, xout, nullptr, static_cast<cudaStream_t>(s));
+}
+void pool_profile_layers(bd_pool* p, const bd_request* r, uint64_t n, const float* xin,
+                         float* xout, double* ms, uint64_t* cnt, void* s) {
+    require((r && xin && xout && ms && cnt) || n == 0, BD_ERR_BAD_ARGUMENT,
+            "profile_layers: null argument");
+    PoolImpl& P = p->impl;
+    P.validate(r, n);
+    P.profiling = true;
+    P.prof_events.clear();
+    try {
+        P.stats.backbone_passes += 1;
+        P.step(r, n, false, xin, xout, nullptr, static_cast<cudaStream_t>(s));
+    } catch (...) {
+        P.profiling = false;
+        throw;
+    }
+    P.profiling = false;
+    BD_CUDA(cudaStreamSynchronize(P.stream));
+    for (int k = 0; k < BD_PROF_KINDS; ++k) {
+        ms[k] = 0.0;
+        cnt[k] = 0;
+    }
+    for (auto& ev : P.prof_events) {
+        float t = 0.0f;
+        BD_CUDA(cudaEventElapsedTime(&t, ev.second.first, ev.second.second));
+        ms[ev.first] += t;
+        cnt[ev.first] += 1;
+        cudaEventDestroy(ev.second.first);
+        cudaEventDestroy(ev.second.second);
+    }
+    P.prof_events.clear();
 }
 void pool_stats(const bd_pool* p, bd_pool_stats* out) {
     *out = p->impl.stats;

