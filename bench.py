@@ -51,7 +51,8 @@ WORKLOADS = {
 }
 PROJ = ["attn_q", "attn_k", "attn_v", "attn_o", "mlp_gate", "mlp_up", "mlp_down"]
 PROF_KINDS = ["gemm_qkv", "gemm_o", "gemm_gu", "gemm_down", "delta_qkv", "delta_o", "delta_gu",
-              "delta_down", "attn", "norm", "silu"]
+              "delta_down", "attn", "norm", "silu", "fused_qkv", "fused_o", "fused_gu", "fused_down",
+              "xq_prep"]
 
 
 def peaks():
@@ -277,6 +278,8 @@ def roofline(res, hbm_peak, peak_kind):
         # K2: weights once + activations + f32 result; K3: every tenant's plane once
         algo[f"gemm_{g}"] = 2 * rows * cols + 2 * B * cols + 4 * B * rows
         algo[f"delta_{g}"] = T * rows * cols / 8 + 2 * B * cols + 4 * B * rows
+        # fused K2+K3: the backbone tile and every tenant's plane once
+        algo[f"fused_{g}"] = 2 * rows * cols + T * rows * cols / 8 + 2 * B * cols + 4 * B * rows
     prof = res["prof"]
     cand = {k: v for k, v in prof.items() if k in algo and v["count"]}
     dom = max(cand, key=lambda k: cand[k]["ms"])

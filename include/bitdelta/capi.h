@@ -185,7 +185,10 @@ int bd_pool_decode_layers(bd_pool* pool, const bd_request* reqs, uint64_t n, con
 enum bd_prof_kind {
     BD_PROF_GEMM_QKV = 0, BD_PROF_GEMM_O, BD_PROF_GEMM_GU, BD_PROF_GEMM_DOWN,
     BD_PROF_DELTA_QKV, BD_PROF_DELTA_O, BD_PROF_DELTA_GU, BD_PROF_DELTA_DOWN,
-    BD_PROF_ATTN, BD_PROF_NORM, BD_PROF_SILU, BD_PROF_KINDS
+    BD_PROF_ATTN, BD_PROF_NORM, BD_PROF_SILU,
+    /* fused K2+K3 kernels (base GEMM + all tenant planes, tensor cores) */
+    BD_PROF_FUSED_QKV, BD_PROF_FUSED_O, BD_PROF_FUSED_GU, BD_PROF_FUSED_DOWN,
+    BD_PROF_XQ_PREP, BD_PROF_KINDS
 };
 int bd_pool_profile_layers(bd_pool* pool, const bd_request* reqs, uint64_t n, const float* x_in,
                            float* x_out, double* ms_out, uint64_t* count_out, void* stream);

@@ -2,6 +2,7 @@
 // the ABI: every entry point maps bd::Failure to its status code and stores the
 // message for bd_last_error(); CUDA errors map to BD_ERR_CUDA.
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <vector>
@@ -79,13 +80,7 @@ void multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int32_
     const GemmPlan g = plan_base_gemm(out_dim, in_dim, batch);
     const CUtensorMap mw = tmap_weights(W, out_dim, in_dim, in_dim);
     const CUtensorMap mx = tmap_acts(X, batch, in_dim, in_dim, g.bn);
-    float* P = nullptr;
-    float* D = nullptr;
-    BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&P), sizeof(float) * g.splits * batch * out_dim, stream));
-    BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&D), sizeof(float) * batch * out_dim, stream));
-    base_gemm_launch(g, mw, mx, P, stream);
     // tenant segmentation: each tenant's plane once for all of its requests
-    std::vector<DeltaUnit> units;
     std::map<int, std::vector<int>> by_t;
     std::vector<int> order;
     for (int b = 0; b < batch; ++b) {
@@ -96,6 +91,83 @@ void multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int32_
         if (!by_t.count(t)) order.push_back(t);
         by_t[t].push_back(b);
     }
+    // ---- fused tensor-core path (K2+K3 in one kernel) when eligible ----
+    static const bool no_fused = std::getenv("BD_NO_FUSED") && std::getenv("BD_NO_FUSED")[0] != '0';
+    bool aligned = in_dim % 128 == 0;
+    for (int t : order) aligned &= (reinterpret_cast<uintptr_t>(tenant_bits[t]) % 16) == 0;
+    if (!no_fused && aligned && !order.empty()) {
+        FusedParams prm{};
+        prm.n_subs = 1;
+        prm.sub_row0[0] = 0;
+        prm.sub_row0[1] = int(out_dim);
+        std::vector<int> xq_row(batch, 0);
+        std::vector<CUtensorMap> maps;
+        int rows = 0, slot = 0;
+        bool ok = true;
+        for (int t : order) {
+            const auto& rq = by_t[t];
+            for (size_t c = 0; c < rq.size(); c += kFusedMaxReq) {
+                if (slot >= kFusedMaxSlots) { ok = false; break; }
+                FusedSlot& fs = prm.slots[slot++];
+                fs.n_req = int(std::min<size_t>(kFusedMaxReq, rq.size() - c));
+                fs.xrow = rows;
+                for (int q = 0; q < fs.n_req; ++q) {
+                    fs.req[q] = rq[c + q];
+                    xq_row[rq[c + q]] = rows + 2 * q;
+                }
+                rows += ((std::max(2 * fs.n_req, 8) + 7) / 8) * 8;
+                fs.alpha[0] = tenant_alpha[t];
+                fs.map_idx[0] = int(maps.size());
+                maps.push_back(tmap_bits(tenant_bits[t], out_dim, in_dim));
+            }
+        }
+        prm.n_slots = slot;
+        if (ok && plan_fused(prm, out_dim, in_dim, batch)) {
+            const uint64_t kpad = uint64_t(prm.kb_total) * kFusedBK;
+            char* ws = nullptr;
+            const size_t sz_p = sizeof(float) * prm.splits * batch * out_dim;
+            // base-only requests get scratch rows past the slots' TMA box
+            for (int b = 0; b < batch; ++b)
+                if (req_tenant == nullptr || req_tenant[b] < 0) xq_row[b] = prm.xq_rows + 2 * b;
+            const size_t sz_q = size_t(prm.xq_rows + 2 * batch) * kpad;
+            const size_t sz_m = maps.size() * sizeof(CUtensorMap);
+            const size_t sz_s = sizeof(int) * batch * 2 * (prm.kb_total + 1);
+            const size_t total = sz_p + sz_q + sz_m + sz_s + sizeof(float) * batch + sizeof(int) * batch + 512;
+            BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), total, stream));
+            char* cur = ws;
+            auto take = [&](size_t n) { char* r = cur; cur += (n + 127) & ~size_t(127); return r; };
+            float* P = reinterpret_cast<float*>(take(sz_p));
+            int8_t* Xq = reinterpret_cast<int8_t*>(take(sz_q));
+            CUtensorMap* dmaps = reinterpret_cast<CUtensorMap*>(take(sz_m));
+            int* qsum = reinterpret_cast<int*>(take(sz_s));
+            float* xscale = reinterpret_cast<float*>(take(sizeof(float) * batch));
+            int* dxr = reinterpret_cast<int*>(take(sizeof(int) * batch));
+            BD_CUDA(cudaMemsetAsync(Xq, 0, sz_q, stream));
+            BD_CUDA(cudaMemcpyAsync(dmaps, maps.data(), sz_m, cudaMemcpyHostToDevice, stream));
+            BD_CUDA(cudaMemcpyAsync(dxr, xq_row.data(), sizeof(int) * batch, cudaMemcpyHostToDevice, stream));
+            BD_CUDA(cudaStreamSynchronize(stream));  // host staging (maps, rows) consumed
+            prm.map_w = mw;
+            prm.map_x = mx;
+            prm.map_xq = tmap_xq(Xq, prm.xq_rows, kpad, kpad);
+            prm.bits_maps = dmaps;
+            prm.xscale = xscale;
+            prm.qsum = qsum;
+            prm.partial = P;
+            xq_prep_launch(X, int(in_dim), int(in_dim), batch, dxr, Xq, int(kpad), xscale, qsum,
+                           prm.kb_total, stream);
+            fused_launch(prm, stream);
+            combine_launch(P, prm.splits, nullptr, batch, int(out_dim), Y, stream);
+            BD_CUDA(cudaFreeAsync(ws, stream));
+            return;
+        }
+    }
+    // ---- SIMT fallback: tcgen05 base GEMM + tenant-segmented delta units ----
+    float* P = nullptr;
+    float* D = nullptr;
+    BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&P), sizeof(float) * g.splits * batch * out_dim, stream));
+    BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&D), sizeof(float) * batch * out_dim, stream));
+    base_gemm_launch(g, mw, mx, P, stream);
+    std::vector<DeltaUnit> units;
     for (int t : order) {
         const auto& rq = by_t[t];
         for (size_t c = 0; c < rq.size(); c += kMaxReqPerUnit) {

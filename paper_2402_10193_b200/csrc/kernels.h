@@ -56,6 +56,45 @@ struct DeltaUnit {
 void delta_units_launch(const DeltaUnit* units_host, int n_units, const void* X, int ldx,
                         int cols, int batch, float* D, int out_rows, cudaStream_t stream);
 
+// ---- K2+K3 fused: base GEMM + tenant deltas on the tensor cores ----
+// The sign planes are expanded in registers to u8 {0,128} A tiles written to
+// TMEM and multiplied (tcgen05.mma kind::i8) with the activations quantised
+// to two int8 fixed-point pieces; see mtfused.cu for the numerics.
+constexpr int kFusedMaxSlots = 32;
+constexpr int kFusedMaxSubs = 3;
+constexpr int kFusedMaxReq = 32;
+struct FusedSlot {
+    int dcol;                    // TMEM column of this slot's s32 accumulator
+    int n;                       // MMA N (8 or a multiple of 16)
+    int xrow;                    // first Xq row (multiple of 8)
+    int n_req;
+    int req[kFusedMaxReq];       // batch indices, pieces at rows xrow + 2q, 2q+1
+    float alpha[kFusedMaxSubs];  // per stacked sub-matrix
+    int map_idx[kFusedMaxSubs];  // index into the bits tensor-map table
+};
+struct FusedParams {
+    CUtensorMap map_w, map_x, map_xq;
+    const CUtensorMap* bits_maps;  // device table
+    const float* xscale;           // [batch] fixed-point scale per request
+    const int* qsum;               // [batch][2][kb_total+1] prefix sums of the pieces
+    float* partial;                // [splits][batch][M]
+    int M, batch, bn, kb_total, kb_per_split, splits, m_tiles, stages, smem;
+    int n_slots, n_subs;
+    int sub_row0[kFusedMaxSubs + 1];
+    int a_col0, tmem_cols, xq_rows;
+    FusedSlot slots[kFusedMaxSlots];
+};
+constexpr int kFusedBK = 128;
+// Fills the tiling fields (bn, stages, splits, TMEM layout) given slots; false if it does not fit.
+bool plan_fused(FusedParams& p, uint64_t M, uint64_t K, int batch);
+void fused_launch(const FusedParams& p, cudaStream_t stream);
+// X bf16 [batch x ldx] -> Xq int8 [xq_rows x ldq] (permuted K, 2 pieces per request at
+// rows xq_row[b], +1), xscale[b], qsum[b][2][kb+1]
+void xq_prep_launch(const void* X, int ldx, int K, int batch, const int* xq_row_dev, int8_t* Xq,
+                    int ldq, float* xscale, int* qsum, int kb_total, cudaStream_t stream);
+CUtensorMap tmap_bits(const uint8_t* bits, uint64_t rows, uint64_t cols);
+CUtensorMap tmap_xq(const int8_t* Xq, int rows, uint64_t K, uint64_t ldq);
+
 // Y[b][m] = sum_s P[s][b][m] (+ D[b][m])
 void combine_launch(const float* P, int splits, const float* D, int batch, int M, float* Y,
                     cudaStream_t stream);

@@ -113,6 +113,18 @@ struct Plan {
     std::vector<DeltaUnit> lm_units;
     GemmPlan g_qkv, g_o, g_gu, g_down, g_lm;
     CUtensorMap x_xn, x_ctx, x_act;  // B-operand maps for this batch size
+    // fused K2+K3 (tensor-core deltas) per layer & group, when eligible
+    struct Fused {
+        bool ok = false;
+        FusedParams prm;
+    };
+    std::vector<std::array<Fused, 4>> fused;
+    int8_t* Xq = nullptr;  // [256 x ldq] int8 pieces (zero padded)
+    int ldq = 0;
+    float* xscale = nullptr;
+    int* qsum = nullptr;
+    int* d_xq_row = nullptr;
+    CUtensorMap m_xq_dim, m_xq_inter;
     cudaGraphExec_t graph_layers = nullptr, graph_full = nullptr;
     uint64_t kernels_layers = 0, kernels_full = 0;
 };
@@ -153,6 +165,7 @@ struct PoolImpl {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     bool use_graphs = true;
+    bool use_fused = true;
 
     ~PoolImpl() {
         cudaSetDevice(device);
@@ -214,6 +227,7 @@ struct PoolImpl {
         BD_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         BD_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
         if (const char* e = std::getenv("BD_NO_GRAPH")) use_graphs = (e[0] == '0');
+        if (const char* e = std::getenv("BD_NO_FUSED")) use_fused = (e[0] == '0');
 
         L.resize(a.n_layers);
         for (auto& l : L) {
@@ -633,6 +647,111 @@ struct PoolImpl {
         logits = dmalloc<float>(ws_B * a.vocab, &ws_allocs);
     }
 
+    // Tensor-core delta path (mtfused.cu) for every projection group whose
+    // shapes allow it (plane rows start on 16-byte TMA boundaries: cols % 128,
+    // stacked sub-matrix boundaries % 128) and whose slots fit TMEM.
+    void plan_fused_groups(Plan& p, const std::vector<int>& order,
+                           std::map<int, std::vector<int>>& by_t) {
+        const int B = p.B;
+        const uint64_t nL = a.n_layers;
+        // Xq rows: each tenant's requests get consecutive rows, 8-row aligned
+        std::vector<int> xq_row(B, 0), t_xrow;
+        int rows = 0;
+        for (int t : order) {
+            const auto& rq = by_t[t];
+            for (size_t c = 0; c < rq.size(); c += kFusedMaxReq) {
+                const int n = int(std::min<size_t>(kFusedMaxReq, rq.size() - c));
+                t_xrow.push_back(rows);
+                for (int q = 0; q < n; ++q) xq_row[rq[c + q]] = rows + 2 * q;
+                const int mma_n = 2 * n <= 8 ? 8 : ((2 * n + 15) / 16) * 16;
+                rows += ((std::max(2 * n, 8) + 7) / 8) * 8;
+                (void)mma_n;
+            }
+        }
+        const uint64_t kpad = round_up(std::max(a.dim, a.intermediate), kFusedBK);
+        p.ldq = int(kpad);
+        const int xq_alloc_rows = 256 + 16;
+        p.Xq = dmalloc<int8_t>(size_t(xq_alloc_rows) * kpad, &p.allocs);
+        BD_CUDA(cudaMemset(p.Xq, 0, size_t(xq_alloc_rows) * kpad));
+        p.xscale = dmalloc<float>(B, &p.allocs);
+        p.qsum = dmalloc<int>(size_t(B) * 2 * (kpad / kFusedBK + 1), &p.allocs);
+        p.d_xq_row = dmalloc<int>(B, &p.allocs);
+        BD_CUDA(cudaMemcpy(p.d_xq_row, xq_row.data(), B * sizeof(int), cudaMemcpyHostToDevice));
+        p.fused.assign(nL, {});
+        struct GroupDef {
+            std::vector<int> projs;
+            uint64_t cols;
+            const CUtensorMap* mx;
+        };
+        const GroupDef defs[4] = {{{P_Q, P_K, P_V}, a.dim, &p.x_xn},
+                                  {{P_O}, a.dim, &p.x_ctx},
+                                  {{P_GATE, P_UP}, a.dim, &p.x_xn},
+                                  {{P_DOWN}, a.intermediate, &p.x_act}};
+        for (int gi = 0; gi < 4; ++gi) {
+            const GroupDef& gd = defs[gi];
+            if (gd.cols % 128) continue;
+            bool ok = true;
+            uint64_t M = 0;
+            std::vector<int> sub_row0;
+            for (int pj : gd.projs) {
+                uint64_t r0, nr;
+                local_rows(pj, r0, nr);
+                if (nr % 128) ok = false;
+                sub_row0.push_back(int(M));
+                M += nr;
+            }
+            sub_row0.push_back(int(M));
+            if (!ok) continue;
+            for (uint64_t l = 0; l < nL && ok; ++l) {
+                FusedParams prm{};
+                prm.n_subs = int(gd.projs.size());
+                for (size_t s = 0; s < sub_row0.size(); ++s) prm.sub_row0[s] = sub_row0[s];
+                std::vector<CUtensorMap> maps;
+                int slot = 0, ti = 0;
+                for (int t : order) {
+                    const auto& rq = by_t[t];
+                    const size_t n_planes = tenants[t].proj[l][gd.projs[0]].size();
+                    for (size_t c = 0; c < rq.size() && ok; c += kFusedMaxReq, ++ti) {
+                        for (size_t k = 0; k < n_planes; ++k) {
+                            if (slot >= kFusedMaxSlots) { ok = false; break; }
+                            FusedSlot& fs = prm.slots[slot++];
+                            fs.n_req = int(std::min<size_t>(kFusedMaxReq, rq.size() - c));
+                            for (int q = 0; q < fs.n_req; ++q) fs.req[q] = rq[c + q];
+                            fs.xrow = t_xrow[ti];
+                            for (size_t s = 0; s < gd.projs.size(); ++s) {
+                                const int pj = gd.projs[s];
+                                const auto& planes = tenants[t].proj[l][pj];
+                                if (planes.size() != n_planes) { ok = false; break; }
+                                uint64_t r0, nr;
+                                local_rows(pj, r0, nr);
+                                fs.alpha[s] = planes[k].alpha;
+                                fs.map_idx[s] = int(maps.size());
+                                maps.push_back(tmap_bits(planes[k].bits, nr, gd.cols));
+                            }
+                        }
+                    }
+                }
+                prm.n_slots = slot;
+                if (!ok || !plan_fused(prm, M, gd.cols, B)) { ok = false; break; }
+                CUtensorMap* dm = dmalloc<CUtensorMap>(maps.size(), &p.allocs);
+                BD_CUDA(cudaMemcpy(dm, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+                prm.bits_maps = dm;
+                prm.map_x = *gd.mx;
+                const LayerW& W = L[l];
+                prm.map_w = gi == 0 ? W.m_qkv : gi == 1 ? W.m_o : gi == 2 ? W.m_gu : W.m_down;
+                prm.map_xq = tmap_xq(p.Xq, prm.xq_rows, round_up(gd.cols, kFusedBK), kpad);
+                prm.xscale = p.xscale;
+                prm.qsum = p.qsum;
+                prm.partial = P;
+                require(uint64_t(prm.splits) * B * M <= P_elems, BD_ERR_CUDA, "split-K workspace too small");
+                p.fused[l][gi].prm = prm;
+                p.fused[l][gi].ok = true;
+            }
+            if (!ok)
+                for (uint64_t l = 0; l < nL; ++l) p.fused[l][gi].ok = false;
+        }
+    }
+
     Plan& plan_for(const std::vector<int>& reqs) {
         std::string key;
         for (int r : reqs) key += std::to_string(r) + ",";
@@ -747,6 +866,7 @@ struct PoolImpl {
         p->x_xn = tmap_acts(xn, B, a.dim, ld_dim, bn);
         p->x_ctx = tmap_acts(ctx, B, a.dim, ld_dim, bn);
         p->x_act = tmap_acts(act, B, a.intermediate, ld_inter, bn);
+        if (use_fused) plan_fused_groups(*p, order, by_t);
         auto& slot = plans[key];
         slot = std::move(p);
         return *slot;
@@ -780,9 +900,34 @@ struct PoolImpl {
         prof_events.push_back({kind, {e0, e1}});
     }
 
-    void linear(int group, const GemmPlan& g, const CUtensorMap& mw, const CUtensorMap& mx,
-                const std::vector<DeltaUnit>& units, const uint16_t* X, int ldx, int cols, int B,
-                cudaStream_t s) {
+    bool fused_ok(const Plan& p, uint64_t l, int gi) const {
+        return p.fused.size() > l && p.fused[l][gi].ok;
+    }
+    ProjOut group_out(const Plan& p, uint64_t l, int gi, const GemmPlan& g) const {
+        if (fused_ok(p, l, gi)) {
+            const FusedParams& f = p.fused[l][gi].prm;
+            ProjOut o;
+            o.P = P;
+            o.splits = f.splits;
+            o.pstride = size_t(p.B) * f.M;
+            o.D = nullptr;
+            o.M = f.M;
+            return o;
+        }
+        return proj_out(g, true);
+    }
+
+    void linear(Plan& p, uint64_t l, int group, const GemmPlan& g, const CUtensorMap& mw,
+                const CUtensorMap& mx, const std::vector<DeltaUnit>& units, const uint16_t* X,
+                int ldx, int cols, int B, cudaStream_t s) {
+        if (fused_ok(p, l, group)) {
+            const FusedParams& f = p.fused[l][group].prm;
+            prof(BD_PROF_XQ_PREP, s, [&] {
+                xq_prep_launch(X, ldx, cols, B, p.d_xq_row, p.Xq, p.ldq, p.xscale, p.qsum, f.kb_total, s);
+            });
+            prof(BD_PROF_FUSED_QKV + group, s, [&] { fused_launch(f, s); });
+            return;
+        }
         prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm_launch(g, mw, mx, P, s); });
         prof(BD_PROF_DELTA_QKV + group, s, [&] {
             delta_units_launch(units.data(), int(units.size()), X, ldx, cols, B, D, int(g.M), s);
@@ -804,23 +949,23 @@ struct PoolImpl {
                 resid_norm_launch(x, B, int(a.dim), prev, p.d_norm + (2 * l) * B, xn, int(ld_dim),
                                   nullptr, s);
             });
-            linear(0, p.g_qkv, W.m_qkv, p.x_xn, p.units[l][0], xn, int(ld_dim), int(a.dim), B, s);
+            linear(p, l, 0, p.g_qkv, W.m_qkv, p.x_xn, p.units[l][0], xn, int(ld_dim), int(a.dim), B, s);
             aa.layer = int(l);
             prof(BD_PROF_ATTN, s, [&] {
-                attn_launch(proj_out(p.g_qkv, true), aa, p.d_pos, B, ctx, int(ld_dim), s);
+                attn_launch(group_out(p, l, 0, p.g_qkv), aa, p.d_pos, B, ctx, int(ld_dim), s);
             });
-            linear(1, p.g_o, W.m_o, p.x_ctx, p.units[l][1], ctx, int(ld_dim), int(a.dim), B, s);
+            linear(p, l, 1, p.g_o, W.m_o, p.x_ctx, p.units[l][1], ctx, int(ld_dim), int(a.dim), B, s);
             prof(BD_PROF_NORM, s, [&] {
-                resid_norm_launch(x, B, int(a.dim), proj_out(p.g_o, true),
+                resid_norm_launch(x, B, int(a.dim), group_out(p, l, 1, p.g_o),
                                   p.d_norm + (2 * l + 1) * B, xn, int(ld_dim), nullptr, s);
             });
-            linear(2, p.g_gu, W.m_gu, p.x_xn, p.units[l][2], xn, int(ld_dim), int(a.dim), B, s);
+            linear(p, l, 2, p.g_gu, W.m_gu, p.x_xn, p.units[l][2], xn, int(ld_dim), int(a.dim), B, s);
             prof(BD_PROF_SILU, s, [&] {
-                silu_launch(proj_out(p.g_gu, true), B, int(a.intermediate), act, int(ld_inter), s);
+                silu_launch(group_out(p, l, 2, p.g_gu), B, int(a.intermediate), act, int(ld_inter), s);
             });
-            linear(3, p.g_down, W.m_down, p.x_act, p.units[l][3], act, int(ld_inter),
+            linear(p, l, 3, p.g_down, W.m_down, p.x_act, p.units[l][3], act, int(ld_inter),
                    int(a.intermediate), B, s);
-            prev = proj_out(p.g_down, true);
+            prev = group_out(p, l, 3, p.g_down);
         }
         prof(BD_PROF_NORM, s, [&] {
             resid_norm_launch(x, B, int(a.dim), prev, nullptr, nullptr, 0, nullptr, s);
