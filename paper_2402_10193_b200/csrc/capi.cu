@@ -91,8 +91,43 @@ void multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int32_
         if (!by_t.count(t)) order.push_back(t);
         by_t[t].push_back(b);
     }
+    static const char* mode_env = std::getenv("BD_DELTA");
+    const std::string mode = mode_env ? mode_env : "auto";
+    size_t max_per_tenant = 0;
+    for (int t : order) max_per_tenant = std::max(max_per_tenant, by_t[t].size());
+    // ---- byte-LUT path (few requests per tenant): tcgen05 base GEMM + K3 LUT ----
+    if ((mode == "lut" || (mode == "auto" && max_per_tenant <= 4)) && !order.empty() &&
+        batch <= kLutMaxJobs) {
+        LutParams prm{};
+        for (int b = 0; b < batch; ++b) {
+            const int t = req_tenant ? req_tenant[b] : -1;
+            if (t < 0) continue;
+            LutJob& j = prm.jobs[prm.n_jobs++];
+            j.req = b;
+            j.n_planes[0] = 1;
+            j.bits[0][0] = tenant_bits[t];
+            j.alpha[0][0] = tenant_alpha[t];
+        }
+        const int seg_rows[1] = {int(out_dim)};
+        if (plan_lut(prm, seg_rows, 1, int(in_dim), int(in_dim), batch)) {
+            float* P = nullptr;
+            float* D = nullptr;
+            BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&P), sizeof(float) * g.splits * batch * out_dim, stream));
+            BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&D), sizeof(float) * prm.slices * batch * out_dim, stream));
+            // base-only requests have no job: their delta slices must read as zero
+            if (size_t(prm.n_jobs) < size_t(batch))
+                BD_CUDA(cudaMemsetAsync(D, 0, sizeof(float) * prm.slices * batch * out_dim, stream));
+            base_gemm_launch(g, mw, mx, P, stream);
+            lut_launch(prm, X, D, stream);
+            combine_launch(P, g.splits, D, batch, int(out_dim), Y, stream, prm.slices);
+            BD_CUDA(cudaFreeAsync(P, stream));
+            BD_CUDA(cudaFreeAsync(D, stream));
+            return;
+        }
+    }
     // ---- fused tensor-core path (K2+K3 in one kernel) when eligible ----
-    static const bool no_fused = std::getenv("BD_NO_FUSED") && std::getenv("BD_NO_FUSED")[0] != '0';
+    static const bool no_fused = (std::getenv("BD_NO_FUSED") && std::getenv("BD_NO_FUSED")[0] != '0') ||
+                                 mode == "units";
     bool aligned = in_dim % 128 == 0;
     for (int t : order) aligned &= (reinterpret_cast<uintptr_t>(tenant_bits[t]) % 16) == 0;
     if (!no_fused && aligned && !order.empty()) {
@@ -102,6 +137,7 @@ void multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int32_
         prm.sub_row0[1] = int(out_dim);
         std::vector<int> xq_row(batch, 0);
         std::vector<CUtensorMap> maps;
+        std::vector<const uint8_t*> map_ptrs;
         int rows = 0, slot = 0;
         bool ok = true;
         for (int t : order) {
@@ -117,8 +153,17 @@ void multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int32_
                 }
                 rows += ((std::max(2 * fs.n_req, 8) + 7) / 8) * 8;
                 fs.alpha[0] = tenant_alpha[t];
-                fs.map_idx[0] = int(maps.size());
-                maps.push_back(tmap_bits(tenant_bits[t], out_dim, in_dim));
+                int mi = -1;  // one descriptor per distinct plane pointer
+                for (int j = 0; j < slot - 1 && mi < 0; ++j)
+                    if (tenant_bits[order[0]] && prm.slots[j].map_idx[0] >= 0 &&
+                        map_ptrs[prm.slots[j].map_idx[0]] == tenant_bits[t])
+                        mi = prm.slots[j].map_idx[0];
+                if (mi < 0) {
+                    mi = int(maps.size());
+                    maps.push_back(tmap_bits(tenant_bits[t], out_dim, in_dim));
+                    map_ptrs.push_back(tenant_bits[t]);
+                }
+                fs.map_idx[0] = mi;
             }
         }
         prm.n_slots = slot;

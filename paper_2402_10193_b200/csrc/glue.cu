@@ -6,8 +6,10 @@
 //     cos/sin come from the same double pow/cos/sin the reference evaluates;
 //   * f32 softmax (nn_ops.hpp:48-57) and SiLU (nn_ops.hpp:59).
 // Each glue kernel also folds in the split-K reduction of the projection that
-// produced its input (sum of base partials + tenant delta), so the linears
-// never make an extra pass over their outputs.
+// produced its input (sum of base partials + tenant delta partials), so the
+// linears never make an extra pass over their outputs. All reductions use a
+// fixed order (no atomics): outputs are bit-reproducible and independent of a
+// request's position in the batch.
 #include <algorithm>
 
 #include "common.cuh"
@@ -19,10 +21,13 @@ void note_launch();
 
 namespace {
 
+constexpr int kNormChunk = 256;  // elements per block in the residual/norm kernels
+
 __device__ __forceinline__ float proj_val(const ProjOut& p, int b, int m) {
     float s = 0.0f;
     for (int k = 0; k < p.splits; ++k) s += p.P[static_cast<size_t>(k) * p.pstride + size_t(b) * p.M + m];
-    if (p.D) s += p.D[size_t(b) * p.M + m];
+    if (p.D)
+        for (int k = 0; k < p.dsplits; ++k) s += p.D[static_cast<size_t>(k) * p.dstride + size_t(b) * p.M + m];
     return s;
 }
 
@@ -54,34 +59,44 @@ __device__ float block_max(float v, float* red) {
     return t;
 }
 
-// one block per request: x += proj (optional); xn = rmsnorm(x) * w_b (optional)
-__global__ void resid_norm_kernel(float* __restrict__ x, int dim, ProjOut proj,
-                                  const float* const* __restrict__ norm_w,
-                                  uint16_t* __restrict__ xn, int ldxn, float* __restrict__ xn_f32) {
+// phase 1, grid (chunks, batch): x += proj (optional); per-chunk sum of squares (double)
+__global__ void __launch_bounds__(kNormChunk)
+    resid_kernel(float* __restrict__ x, int dim, ProjOut proj, double* __restrict__ msq_part) {
     __shared__ double red_d[32];
-    const int b = blockIdx.x;
-    float* xb = x + size_t(b) * dim;
-    double msq = 0.0;
-    for (int i = threadIdx.x; i < dim; i += blockDim.x) {
-        float v = xb[i];
+    const int b = blockIdx.y;
+    const int i = blockIdx.x * kNormChunk + threadIdx.x;
+    double sq = 0.0;
+    if (i < dim) {
+        float v = x[size_t(b) * dim + i];
         if (proj.P) {
             v = v + proj_val(proj, b, proj.col0 + i);
-            xb[i] = v;
+            x[size_t(b) * dim + i] = v;
         }
-        msq += static_cast<double>(v) * v;
+        sq = static_cast<double>(v) * v;
     }
-    if (!norm_w) return;
-    msq = block_sum(msq, red_d);
-    const double inv = 1.0 / sqrt(msq / static_cast<double>(dim) + 1e-12);
-    const float* w = norm_w[b];
-    for (int i = threadIdx.x; i < dim; i += blockDim.x) {
-        const float y = static_cast<float>(static_cast<double>(xb[i]) * inv) * w[i];
-        if (xn) xn[size_t(b) * ldxn + i] = f32_to_bf16(y);
-        if (xn_f32) xn_f32[size_t(b) * dim + i] = y;
-    }
+    if (!msq_part) return;
+    sq = block_sum(sq, red_d);
+    if (threadIdx.x == 0) msq_part[size_t(b) * gridDim.x + blockIdx.x] = sq;
 }
 
-// one block per (head, request)
+// phase 2, grid (chunks, batch): xn = rmsnorm(x) * w_b  (every block re-sums the
+// chunk partials of its request in index order -> deterministic)
+__global__ void __launch_bounds__(kNormChunk)
+    norm_kernel(const float* __restrict__ x, int dim, const double* __restrict__ msq_part,
+                const float* const* __restrict__ norm_w, uint16_t* __restrict__ xn, int ldxn,
+                float* __restrict__ xn_f32) {
+    const int b = blockIdx.y;
+    const int i = blockIdx.x * kNormChunk + threadIdx.x;
+    double msq = 0.0;
+    for (int k = 0; k < int(gridDim.x); ++k) msq += msq_part[size_t(b) * gridDim.x + k];
+    const double inv = 1.0 / sqrt(msq / static_cast<double>(dim) + 1e-12);
+    if (i >= dim) return;
+    const float y = static_cast<float>(static_cast<double>(x[size_t(b) * dim + i]) * inv) * norm_w[b][i];
+    if (xn) xn[size_t(b) * ldxn + i] = f32_to_bf16(y);
+    if (xn_f32) xn_f32[size_t(b) * dim + i] = y;
+}
+
+// one block per (head, request): RoPE, KV append, scores, softmax, context
 __global__ void attn_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos_dev,
                             uint16_t* __restrict__ ctx_out, int ld_ctx) {
     extern __shared__ float sm[];
@@ -119,21 +134,31 @@ __global__ void attn_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos
             vc[static_cast<size_t>(pos) * a.kv_dim + i] = f32_to_bf16(vs[i]);
         }
     }
-    // scores (serve.cpp:267-275): one warp per key
+    // scores (serve.cpp:267-275): one thread per key, 16-byte loads of the key row
     const int n_ctx = pos + 1;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const float inv_sqrt_hd = 1.0f / sqrtf(static_cast<float>(hd));
-    for (int j = warp; j < n_ctx; j += nw) {
+    const bool vec = (hd % 8) == 0 && (a.kv_dim % 8) == 0;
+    for (int j = threadIdx.x; j < n_ctx; j += blockDim.x) {
         float acc = 0.0f;
         if (j == pos) {
-            for (int d = lane; d < hd; d += 32) acc += qs[d] * ks[d];
+            for (int d = 0; d < hd; ++d) acc += qs[d] * ks[d];
+        } else if (vec) {
+            const uint4* kj = reinterpret_cast<const uint4*>(kc + static_cast<size_t>(j) * a.kv_dim);
+#pragma unroll 4
+            for (int d8 = 0; d8 < hd / 8; ++d8) {
+                const uint4 u = kj[d8];
+                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    acc += qs[8 * d8 + 2 * e] * __uint_as_float(w[e] << 16);
+                    acc += qs[8 * d8 + 2 * e + 1] * __uint_as_float(w[e] & 0xFFFF0000u);
+                }
+            }
         } else {
             const uint16_t* kj = kc + static_cast<size_t>(j) * a.kv_dim;
-            for (int d = lane; d < hd; d += 32) acc += qs[d] * bf16_to_f32(kj[d]);
+            for (int d = 0; d < hd; ++d) acc += qs[d] * bf16_to_f32(kj[d]);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) scores[j] = acc * inv_sqrt_hd;
+        scores[j] = acc * inv_sqrt_hd;
     }
     __syncthreads();
     // softmax (nn_ops.hpp:48-57)
@@ -148,11 +173,14 @@ __global__ void attn_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos
     }
     sum = block_sum(sum, red);
     __syncthreads();
-    // ctx (serve.cpp:276-281): sequential over positions, like the reference
+    // ctx (serve.cpp:276-281): sequential over positions, like the reference;
+    // value rows read coalesced across the threads of the block
     for (int d = threadIdx.x; d < hd; d += blockDim.x) {
         float acc = 0.0f;
+        const uint16_t* vcol = vc + d;
+#pragma unroll 8
         for (int j = 0; j < n_ctx; ++j) {
-            const float v = (j == pos) ? vs[d] : bf16_to_f32(vc[static_cast<size_t>(j) * a.kv_dim + d]);
+            const float v = (j == pos) ? vs[d] : bf16_to_f32(vcol[static_cast<size_t>(j) * a.kv_dim]);
             acc += (scores[j] / sum) * v;
         }
         ctx_out[size_t(b) * ld_ctx + h * hd + d] = f32_to_bf16(acc);
@@ -203,9 +231,16 @@ __global__ void logits_kernel(ProjOut lm, const float* const* __restrict__ raw_d
 
 }  // namespace
 
+int norm_chunks(int dim) { return (dim + kNormChunk - 1) / kNormChunk; }
+
 void resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const float* const* norm_w,
-                       uint16_t* xn, int ldxn, float* xn_f32, cudaStream_t s) {
-    resid_norm_kernel<<<batch, 256, 0, s>>>(x, dim, proj, norm_w, xn, ldxn, xn_f32);
+                       uint16_t* xn, int ldxn, float* xn_f32, double* msq_ws, cudaStream_t s) {
+    const dim3 grid(norm_chunks(dim), batch);
+    resid_kernel<<<grid, kNormChunk, 0, s>>>(x, dim, proj, norm_w ? msq_ws : nullptr);
+    note_launch();
+    BD_CUDA(cudaGetLastError());
+    if (!norm_w) return;
+    norm_kernel<<<grid, kNormChunk, 0, s>>>(x, dim, msq_ws, norm_w, xn, ldxn, xn_f32);
     note_launch();
     BD_CUDA(cudaGetLastError());
 }

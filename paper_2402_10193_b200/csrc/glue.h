@@ -12,7 +12,9 @@ struct ProjOut {
     const float* P = nullptr;
     int splits = 0;
     size_t pstride = 0;
-    const float* D = nullptr;
+    const float* D = nullptr;  // delta partials: sum_{k < dsplits} D[k*pstride_d + b*M + m]
+    int dsplits = 1;
+    size_t dstride = 0;
     int M = 0;
     int col0 = 0;  // column offset used by resid_norm (o / down outputs)
 };
@@ -24,8 +26,10 @@ struct AttnArgs {
     const float2* rope;       // [max_seq][hd/2] (cos, sin)
 };
 
+// msq_ws: batch * norm_chunks(dim) doubles of scratch
+int norm_chunks(int dim);
 void resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const float* const* norm_w,
-                       uint16_t* xn, int ldxn, float* xn_f32, cudaStream_t s);
+                       uint16_t* xn, int ldxn, float* xn_f32, double* msq_ws, cudaStream_t s);
 void attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int batch,
                  uint16_t* ctx, int ld_ctx, cudaStream_t s);
 void silu_launch(const ProjOut& gu, int batch, int inter, uint16_t* act, int ld_act, cudaStream_t s);

@@ -82,6 +82,8 @@ struct FusedParams {
     int n_slots, n_subs;
     int sub_row0[kFusedMaxSubs + 1];
     int a_col0, tmem_cols, xq_rows;
+    int ring;   // TMEM A-operand ring entries (32 columns each)
+    int debug;  // experiment flags (0 in production)
     FusedSlot slots[kFusedMaxSlots];
 };
 constexpr int kFusedBK = 128;
@@ -95,8 +97,29 @@ void xq_prep_launch(const void* X, int ldx, int K, int batch, const int* xq_row_
 CUtensorMap tmap_bits(const uint8_t* bits, uint64_t rows, uint64_t cols);
 CUtensorMap tmap_xq(const int8_t* Xq, int rows, uint64_t K, uint64_t ldq);
 
+// ---- K3 byte-LUT (few requests per tenant; lut.cu) ----
+constexpr int kLutMaxSegs = 3;
+constexpr int kLutMaxChunks = 48;
+constexpr int kLutMaxJobs = 64;
+struct LutJob {
+    int req;                                              // batch index
+    int n_planes[kLutMaxSegs];
+    const uint8_t* bits[kLutMaxSegs][kMaxPlanesPerUnit];  // reference layout, cols % 32 == 0
+    float alpha[kLutMaxSegs][kMaxPlanesPerUnit];
+};
+struct LutParams {
+    int n_jobs, slices, n_chunks, cols, ldx, batch, M;
+    int seg_row0[kLutMaxSegs];
+    int chunk_seg[kLutMaxChunks], chunk_begin[kLutMaxChunks], chunk_end[kLutMaxChunks];
+    LutJob jobs[kLutMaxJobs];
+};
+// Chunking of the stacked rows (seg_rows) into CTAs; returns false if unsupported.
+bool plan_lut(LutParams& p, const int* seg_rows, int n_segs, int cols, int ldx, int batch);
+// out: [slices][batch][M] f32, alpha already applied; every (slice, req, row) of a job written
+void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream);
+
 // Y[b][m] = sum_s P[s][b][m] (+ D[b][m])
 void combine_launch(const float* P, int splits, const float* D, int batch, int M, float* Y,
-                    cudaStream_t stream);
+                    cudaStream_t stream, int dsplits = 1);
 
 }  // namespace bd

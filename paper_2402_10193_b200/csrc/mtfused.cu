@@ -30,6 +30,7 @@
 // Split-K partials are written (not atomically added): bit-reproducible.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -41,7 +42,7 @@ void note_launch();
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kRing = 4;        // TMEM A slots
+constexpr int kMaxRing = 12;    // TMEM A slots (runtime p.ring <= kMaxRing)
 constexpr int kMaxStages = 4;
 constexpr int kBitsBox = 16;    // bytes of one plane row per stage (128 bits)
 
@@ -68,8 +69,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * L.stage);
     uint64_t* empty = full + kMaxStages;
     uint64_t* a_full = empty + kMaxStages;
-    uint64_t* a_empty = a_full + kRing;
-    uint64_t* done = a_empty + kRing;
+    uint64_t* a_empty = a_full + kMaxRing;
+    uint64_t* done = a_empty + kMaxRing;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
     float* ys = reinterpret_cast<float*>(smem);  // epilogue staging (reuses stage 0)
 
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        for (int r = 0; r < kRing; ++r) {
+        for (int r = 0; r < p.ring; ++r) {
             mbar_init(&a_full[r], 128);
             mbar_init(&a_empty[r], 1);
         }
@@ -142,6 +143,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
                 mbar_wait(&full[s], (i / p.stages) & 1);
                 tc_fence_after();
                 uint8_t* st = smem + s * L.stage;
+                if (!(p.debug & 8))
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     const uint64_t da = sdesc_k128(st + L.w_off + (k >> 2) * 128 * 128) + 2 * (k & 3);
@@ -149,12 +151,13 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
                     mma_bf16_ss(tbase, da, db, id_base, (i > 0 || k > 0) ? 1u : 0u);
                 }
                 for (int j = 0; j < p.n_slots; ++j, ++g) {
-                    const int r = g % kRing;
-                    mbar_wait(&a_full[r], (g / kRing) & 1);
+                    const int r = g % p.ring;
+                    mbar_wait(&a_full[r], (g / p.ring) & 1);
                     tc_fence_after();
                     const FusedSlot& sl = p.slots[j];
                     const uint32_t id_q = idesc_u8s8_s32(128, sl.n);
                     const uint64_t dq = sdesc_k128(st + L.q_off + sl.xrow * 128);
+                    if (!(p.debug & 4))
 #pragma unroll
                     for (int k = 0; k < 4; ++k)  // K = 32 bytes per MMA
                         mma_i8_ts(tbase + sl.dcol, tbase + p.a_col0 + r * 32 + 8 * k, dq + 2 * k, id_q,
@@ -175,8 +178,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
             mbar_wait(&full[s], (i / p.stages) & 1);
             const uint8_t* bits = smem + s * L.stage + L.bits_off;
             for (int j = 0; j < p.n_slots; ++j, ++g) {
-                const int r = g % kRing;
-                mbar_wait(&a_empty[r], ((g / kRing) & 1) ^ 1);
+                const int r = g % p.ring;
+                mbar_wait(&a_empty[r], ((g / p.ring) & 1) ^ 1);
                 const uint4 w = *reinterpret_cast<const uint4*>(bits + j * 128 * kBitsBox + trow * kBitsBox);
                 const uint32_t wq[4] = {w.x, w.y, w.z, w.w};
                 uint32_t a[32];
@@ -184,8 +187,13 @@ __global__ void __launch_bounds__(kThreads, 1) fused_kernel(const __grid_constan
                 for (int q = 0; q < 4; ++q)
 #pragma unroll
                     for (int c = 0; c < 8; ++c) a[8 * q + c] = (wq[q] << (7 - c)) & 0x80808080u;
-                tmem_st32(tbase + lane_base + p.a_col0 + r * 32, a);
-                tmem_st_wait();
+                if (p.debug & 1)
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) a[c] = 0;
+                if (!(p.debug & 2)) {
+                    tmem_st32(tbase + lane_base + p.a_col0 + r * 32, a);
+                    tmem_st_wait();
+                }
                 tc_fence_before();
                 mbar_arrive(&a_full[r]);
             }
@@ -331,7 +339,11 @@ bool plan_fused(FusedParams& p, uint64_t M, uint64_t K, int batch) {
     }
     col = (col + 31) & ~31;
     p.a_col0 = col;
-    col += kRing * 32;
+    p.ring = std::min(kMaxRing, (512 - col) / 32);
+    if (const char* e = std::getenv("BD_FUSED_RING")) p.ring = std::max(1, std::min(p.ring, atoi(e)));
+    if (p.ring < 2) return false;
+    col += p.ring * 32;
+    p.debug = std::getenv("BD_FUSED_DEBUG") ? atoi(std::getenv("BD_FUSED_DEBUG")) : 0;
     if (col > 512) return false;
     p.tmem_cols = col <= 128 ? 128 : (col <= 256 ? 256 : 512);
     // Xq rows: each slot reads n rows from its xrow (which the caller set, multiple of 8)

@@ -159,13 +159,15 @@ __global__ void __launch_bounds__(kDuThreads)
 }
 
 __global__ void combine_kernel(const float* __restrict__ P, int splits, const float* __restrict__ D,
-                               int batch, int M, float* __restrict__ Y) {
+                               int dsplits, int batch, int M, float* __restrict__ Y) {
     const size_t n = static_cast<size_t>(batch) * M;
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
          i += size_t(gridDim.x) * blockDim.x) {
         float s = 0.0f;
         for (int k = 0; k < splits; ++k) s += P[k * n + i];
-        Y[i] = D ? s + D[i] : s;
+        if (D)
+            for (int k = 0; k < dsplits; ++k) s += D[k * n + i];
+        Y[i] = s;
     }
 }
 
@@ -247,10 +249,10 @@ void delta_units_launch(const DeltaUnit* units, int n_units, const void* X, int 
 }
 
 void combine_launch(const float* P, int splits, const float* D, int batch, int M, float* Y,
-                    cudaStream_t stream) {
+                    cudaStream_t stream, int dsplits) {
     const size_t n = static_cast<size_t>(batch) * M;
     const unsigned grid = static_cast<unsigned>(std::min<size_t>((n + 255) / 256, kNumSMs * 8));
-    combine_kernel<<<grid, 256, 0, stream>>>(P, splits, D, batch, M, Y);
+    combine_kernel<<<grid, 256, 0, stream>>>(P, splits, D, dsplits, batch, M, Y);
     note_launch();
     BD_CUDA(cudaGetLastError());
 }

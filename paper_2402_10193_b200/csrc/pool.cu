@@ -119,6 +119,12 @@ struct Plan {
         FusedParams prm;
     };
     std::vector<std::array<Fused, 4>> fused;
+    // byte-LUT deltas (few requests per tenant) per layer & group
+    struct Lut {
+        bool ok = false;
+        LutParams prm;
+    };
+    std::vector<std::array<Lut, 4>> lut;
     int8_t* Xq = nullptr;  // [256 x ldq] int8 pieces (zero padded)
     int ldq = 0;
     float* xscale = nullptr;
@@ -157,6 +163,7 @@ struct PoolImpl {
     // workspaces (sized for ws_B)
     int ws_B = 0;
     float *x = nullptr, *xn_f32 = nullptr, *P = nullptr, *D = nullptr, *logits = nullptr;
+    double* msq = nullptr;  // per-request chunk sums of squares (RMSNorm)
     uint16_t *xn = nullptr, *ctx = nullptr, *act = nullptr;
     size_t P_elems = 0, D_elems = 0;
     std::vector<void*> ws_allocs;
@@ -166,6 +173,7 @@ struct PoolImpl {
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     bool use_graphs = true;
     bool use_fused = true;
+    std::string delta_mode = "auto";  // auto | lut | fused | units (BD_DELTA)
 
     ~PoolImpl() {
         cudaSetDevice(device);
@@ -228,6 +236,8 @@ struct PoolImpl {
         BD_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
         if (const char* e = std::getenv("BD_NO_GRAPH")) use_graphs = (e[0] == '0');
         if (const char* e = std::getenv("BD_NO_FUSED")) use_fused = (e[0] == '0');
+        if (!use_fused) delta_mode = "units";
+        if (const char* e = std::getenv("BD_DELTA")) delta_mode = e;
 
         L.resize(a.n_layers);
         for (auto& l : L) {
@@ -639,12 +649,67 @@ struct PoolImpl {
         BD_CUDA(cudaMemset(xn, 0, ws_B * ld_dim * 2));
         BD_CUDA(cudaMemset(ctx, 0, ws_B * ld_dim * 2));
         BD_CUDA(cudaMemset(act, 0, ws_B * ld_inter * 2));
-        D_elems = ws_B * Mmax;
+        // delta partials: up to one per 1024-column slice (LUT path)
+        D_elems = ws_B * Mmax * ((std::max(a.dim, a.intermediate) + 1023) / 1024);
         D = dmalloc<float>(D_elems, &ws_allocs);
         // split-K partials: bound by the planner's worst case (<= 32 splits)
         P_elems = 33ull * ws_B * Mmax;
         P = dmalloc<float>(P_elems, &ws_allocs);
         logits = dmalloc<float>(ws_B * a.vocab, &ws_allocs);
+        msq = dmalloc<double>(size_t(ws_B) * norm_chunks(int(a.dim)), &ws_allocs);
+    }
+
+    // Byte-LUT delta path (lut.cu): one job per request, planes read in the
+    // reference layout with coalesced row loads. Used when tenants have few
+    // requests each (the tensor-core path amortises expansion over many).
+    void plan_lut_groups(Plan& p) {
+        const int B = p.B;
+        const uint64_t nL = a.n_layers;
+        if (B > kLutMaxJobs) return;
+        p.lut.assign(nL, {});
+        struct GroupDef {
+            std::vector<int> projs;
+            uint64_t cols, ldx;
+        };
+        const GroupDef defs[4] = {{{P_Q, P_K, P_V}, a.dim, ld_dim},
+                                  {{P_O}, a.dim, ld_dim},
+                                  {{P_GATE, P_UP}, a.dim, ld_dim},
+                                  {{P_DOWN}, a.intermediate, ld_inter}};
+        for (int gi = 0; gi < 4; ++gi) {
+            const GroupDef& gd = defs[gi];
+            int seg_rows[kLutMaxSegs];
+            for (size_t s = 0; s < gd.projs.size(); ++s) {
+                uint64_t r0, nr;
+                local_rows(gd.projs[s], r0, nr);
+                seg_rows[s] = int(nr);
+            }
+            bool ok = true;
+            for (uint64_t l = 0; l < nL && ok; ++l) {
+                LutParams prm{};
+                prm.n_jobs = B;
+                for (int b = 0; b < B; ++b) {
+                    LutJob& j = prm.jobs[b];
+                    j.req = b;
+                    const Tenant& t = tenants[requests[p.reqs[b]].tenant];
+                    for (size_t s = 0; s < gd.projs.size(); ++s) {
+                        const auto& planes = t.proj[l][gd.projs[s]];
+                        j.n_planes[s] = int(planes.size());
+                        for (size_t k = 0; k < planes.size(); ++k) {
+                            j.bits[s][k] = planes[k].bits;
+                            j.alpha[s][k] = planes[k].alpha;
+                        }
+                    }
+                }
+                ok = plan_lut(prm, seg_rows, int(gd.projs.size()), int(gd.cols), int(gd.ldx), B);
+                if (ok && size_t(prm.slices) * B * prm.M > D_elems) ok = false;
+                if (ok) {
+                    p.lut[l][gi].prm = prm;
+                    p.lut[l][gi].ok = true;
+                }
+            }
+            if (!ok)
+                for (uint64_t l = 0; l < nL; ++l) p.lut[l][gi].ok = false;
+        }
     }
 
     // Tensor-core delta path (mtfused.cu) for every projection group whose
@@ -690,6 +755,7 @@ struct PoolImpl {
         for (int gi = 0; gi < 4; ++gi) {
             const GroupDef& gd = defs[gi];
             if (gd.cols % 128) continue;
+            if (!p.lut.empty() && p.lut[0][gi].ok) continue;  // LUT path already chosen
             bool ok = true;
             uint64_t M = 0;
             std::vector<int> sub_row0;
@@ -866,7 +932,10 @@ struct PoolImpl {
         p->x_xn = tmap_acts(xn, B, a.dim, ld_dim, bn);
         p->x_ctx = tmap_acts(ctx, B, a.dim, ld_dim, bn);
         p->x_act = tmap_acts(act, B, a.intermediate, ld_inter, bn);
-        if (use_fused) plan_fused_groups(*p, order, by_t);
+        size_t max_per_tenant = 0;
+        for (int t : order) max_per_tenant = std::max(max_per_tenant, by_t[t].size());
+        if (delta_mode == "lut" || (delta_mode == "auto" && max_per_tenant <= 4)) plan_lut_groups(*p);
+        if (delta_mode == "fused" || delta_mode == "auto") plan_fused_groups(*p, order, by_t);
         auto& slot = plans[key];
         slot = std::move(p);
         return *slot;
@@ -878,6 +947,8 @@ struct PoolImpl {
         o.splits = g.splits;
         o.pstride = size_t(g.batch) * g.M;
         o.D = with_delta ? D : nullptr;
+        o.dsplits = 1;
+        o.dstride = size_t(g.batch) * g.M;
         o.M = int(g.M);
         return o;
     }
@@ -903,7 +974,13 @@ struct PoolImpl {
     bool fused_ok(const Plan& p, uint64_t l, int gi) const {
         return p.fused.size() > l && p.fused[l][gi].ok;
     }
+    bool lut_ok(const Plan& p, uint64_t l, int gi) const { return p.lut.size() > l && p.lut[l][gi].ok; }
     ProjOut group_out(const Plan& p, uint64_t l, int gi, const GemmPlan& g) const {
+        if (lut_ok(p, l, gi)) {
+            ProjOut o = proj_out(g, true);
+            o.dsplits = p.lut[l][gi].prm.slices;
+            return o;
+        }
         if (fused_ok(p, l, gi)) {
             const FusedParams& f = p.fused[l][gi].prm;
             ProjOut o;
@@ -920,6 +997,11 @@ struct PoolImpl {
     void linear(Plan& p, uint64_t l, int group, const GemmPlan& g, const CUtensorMap& mw,
                 const CUtensorMap& mx, const std::vector<DeltaUnit>& units, const uint16_t* X,
                 int ldx, int cols, int B, cudaStream_t s) {
+        if (lut_ok(p, l, group)) {
+            prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm_launch(g, mw, mx, P, s); });
+            prof(BD_PROF_DELTA_QKV + group, s, [&] { lut_launch(p.lut[l][group].prm, X, D, s); });
+            return;
+        }
         if (fused_ok(p, l, group)) {
             const FusedParams& f = p.fused[l][group].prm;
             prof(BD_PROF_XQ_PREP, s, [&] {
@@ -947,7 +1029,7 @@ struct PoolImpl {
             // x += down(prev); xn = norm1(x)
             prof(BD_PROF_NORM, s, [&] {
                 resid_norm_launch(x, B, int(a.dim), prev, p.d_norm + (2 * l) * B, xn, int(ld_dim),
-                                  nullptr, s);
+                                  nullptr, msq, s);
             });
             linear(p, l, 0, p.g_qkv, W.m_qkv, p.x_xn, p.units[l][0], xn, int(ld_dim), int(a.dim), B, s);
             aa.layer = int(l);
@@ -957,7 +1039,7 @@ struct PoolImpl {
             linear(p, l, 1, p.g_o, W.m_o, p.x_ctx, p.units[l][1], ctx, int(ld_dim), int(a.dim), B, s);
             prof(BD_PROF_NORM, s, [&] {
                 resid_norm_launch(x, B, int(a.dim), group_out(p, l, 1, p.g_o),
-                                  p.d_norm + (2 * l + 1) * B, xn, int(ld_dim), nullptr, s);
+                                  p.d_norm + (2 * l + 1) * B, xn, int(ld_dim), nullptr, msq, s);
             });
             linear(p, l, 2, p.g_gu, W.m_gu, p.x_xn, p.units[l][2], xn, int(ld_dim), int(a.dim), B, s);
             prof(BD_PROF_SILU, s, [&] {
@@ -968,7 +1050,7 @@ struct PoolImpl {
             prev = group_out(p, l, 3, p.g_down);
         }
         prof(BD_PROF_NORM, s, [&] {
-            resid_norm_launch(x, B, int(a.dim), prev, nullptr, nullptr, 0, nullptr, s);
+            resid_norm_launch(x, B, int(a.dim), prev, nullptr, nullptr, 0, nullptr, msq, s);
         });
     }
 
@@ -977,7 +1059,7 @@ struct PoolImpl {
         embed_launch(embed, p.d_tok, p.d_embed, B, int(a.dim), x, s);
         run_layers(p, s);
         resid_norm_launch(x, B, int(a.dim), ProjOut{}, p.d_norm + (2 * a.n_layers) * B, xn,
-                          int(ld_dim), xn_f32, s);
+                          int(ld_dim), xn_f32, msq, s);
         base_gemm_launch(p.g_lm, m_lm, p.x_xn, P, s);
         delta_units_launch(p.lm_units.data(), int(p.lm_units.size()), xn, int(ld_dim), int(a.dim),
                            B, D, int(a.vocab), s);

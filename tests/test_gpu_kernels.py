@@ -1,6 +1,8 @@
 """GPU parity of the kernels behind the C-ABI (K1 compress, K3 packed apply,
 K2+K3 multi-tenant linear) against the oracle / golden vectors from the
 reference. Bit-exact for bits; tolerances stated per test."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -201,3 +203,35 @@ def test_multitenant_linear_permutation_bit_identical(cuda):
     perm = list(reversed(range(B)))
     Yp = bd.multitenant_linear(W, bits_list, alphas, [rt[p] for p in perm], X[perm].contiguous())
     assert torch.equal(Yp, Y[perm])
+
+
+@pytest.mark.parametrize("mode", ["lut", "fused", "units"])
+def test_multitenant_linear_each_delta_path(cuda, mode):
+    """Every K3 variant (byte-LUT, tensor-core fused, SIMT units) against the same f64 reference."""
+    import subprocess
+    import sys
+
+    code = f"""
+import sys; sys.path.insert(0, {repr(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))})
+sys.path.insert(0, {repr(os.path.dirname(os.path.abspath(__file__)))})
+import torch, numpy as np
+import paper_2402_10193_b200 as bd
+from test_gpu_kernels import _mt_reference, rel_l2
+dev = torch.device('cuda:0')
+for rows, cols, B, T in [(4096, 4096, 16, 16), (768, 11008, 8, 2), (1024, 2048, 12, 3)]:
+    torch.manual_seed(rows + B)
+    W = (torch.randn(rows, cols, device=dev) * 0.02).to(torch.bfloat16)
+    X = torch.randn(B, cols, device=dev).to(torch.bfloat16)
+    bits, al = [], []
+    for t in range(T):
+        b, a = bd.compress_tensor(W, (W.float() + 1e-3 * torch.randn_like(W.float())).to(torch.bfloat16))
+        bits.append(b); al.append(a.item())
+    rt = [b % T for b in range(B)]
+    Y = bd.multitenant_linear(W, bits, al, rt, X)
+    err = rel_l2(Y.cpu().numpy(), _mt_reference(W, bits, al, rt, X, rows, cols).cpu().numpy())
+    assert err <= 1e-5, (rows, cols, B, T, err)
+print('ok')
+"""
+    env = dict(os.environ, BD_DELTA=mode)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
