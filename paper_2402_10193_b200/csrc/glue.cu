@@ -112,19 +112,29 @@ __global__ void attn_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos
     const int pos = pos_dev[b];
     const float2* rope = a.rope + static_cast<size_t>(pos) * half;
 
-    // q, k, v of this step (split-K reduction + tenant delta), RoPE on q and k
-    for (int i = threadIdx.x; i < half; i += blockDim.x) {
-        const float2 cs = rope[i];
-        const float q0 = proj_val(qkv, b, h * hd + 2 * i), q1 = proj_val(qkv, b, h * hd + 2 * i + 1);
-        qs[2 * i] = q0 * cs.x - q1 * cs.y;
-        qs[2 * i + 1] = q0 * cs.y + q1 * cs.x;
-        const int kc = a.dim + kh * hd;
-        const float k0 = proj_val(qkv, b, kc + 2 * i), k1 = proj_val(qkv, b, kc + 2 * i + 1);
-        ks[2 * i] = bf16_to_f32(f32_to_bf16(k0 * cs.x - k1 * cs.y));
-        ks[2 * i + 1] = bf16_to_f32(f32_to_bf16(k0 * cs.y + k1 * cs.x));
+    // q, k, v of this step (split-K reduction + tenant delta): one element per
+    // thread over all 3*hd values, then RoPE on the q and k pairs in smem
+    for (int i = threadIdx.x; i < 3 * hd; i += blockDim.x) {
+        const int which = i / hd, d = i - which * hd;
+        const int col = which == 0 ? h * hd + d : (which == 1 ? a.dim + kh * hd + d : a.dim + a.kv_dim + kh * hd + d);
+        const float v = proj_val(qkv, b, col);
+        (which == 0 ? qs : (which == 1 ? ks : vs))[d] = which == 2 ? bf16_to_f32(f32_to_bf16(v)) : v;
     }
-    for (int i = threadIdx.x; i < hd; i += blockDim.x)
-        vs[i] = bf16_to_f32(f32_to_bf16(proj_val(qkv, b, a.dim + a.kv_dim + kh * hd + i)));
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2 * half; i += blockDim.x) {
+        const int pi = i % half;
+        float* buf = i < half ? qs : ks;
+        const float2 cs = rope[pi];
+        const float v0 = buf[2 * pi], v1 = buf[2 * pi + 1];
+        const float r0 = v0 * cs.x - v1 * cs.y, r1 = v0 * cs.y + v1 * cs.x;
+        if (i < half) {
+            buf[2 * pi] = r0;
+            buf[2 * pi + 1] = r1;
+        } else {
+            buf[2 * pi] = bf16_to_f32(f32_to_bf16(r0));
+            buf[2 * pi + 1] = bf16_to_f32(f32_to_bf16(r1));
+        }
+    }
     __syncthreads();
     uint16_t* kc = a.kcache[b] + (static_cast<size_t>(a.layer) * a.max_seq) * a.kv_dim + kh * hd;
     uint16_t* vc = a.vcache[b] + (static_cast<size_t>(a.layer) * a.max_seq) * a.kv_dim + kh * hd;
@@ -134,31 +144,30 @@ __global__ void attn_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos
             vc[static_cast<size_t>(pos) * a.kv_dim + i] = f32_to_bf16(vs[i]);
         }
     }
-    // scores (serve.cpp:267-275): one thread per key, 16-byte loads of the key row
+    // scores (serve.cpp:267-275): one warp per key, lane l owns dims [4l, 4l+4) (+128k),
+    // 8-byte loads -> each key row is one coalesced 256-byte warp access
     const int n_ctx = pos + 1;
     const float inv_sqrt_hd = 1.0f / sqrtf(static_cast<float>(hd));
-    const bool vec = (hd % 8) == 0 && (a.kv_dim % 8) == 0;
-    for (int j = threadIdx.x; j < n_ctx; j += blockDim.x) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const bool vec = (hd % 4) == 0 && (a.kv_dim % 4) == 0;
+    for (int j = warp; j < n_ctx; j += nw) {
         float acc = 0.0f;
         if (j == pos) {
-            for (int d = 0; d < hd; ++d) acc += qs[d] * ks[d];
+            for (int d = lane; d < hd; d += 32) acc += qs[d] * ks[d];
         } else if (vec) {
-            const uint4* kj = reinterpret_cast<const uint4*>(kc + static_cast<size_t>(j) * a.kv_dim);
-#pragma unroll 4
-            for (int d8 = 0; d8 < hd / 8; ++d8) {
-                const uint4 u = kj[d8];
-                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    acc += qs[8 * d8 + 2 * e] * __uint_as_float(w[e] << 16);
-                    acc += qs[8 * d8 + 2 * e + 1] * __uint_as_float(w[e] & 0xFFFF0000u);
-                }
+            const uint16_t* kj = kc + static_cast<size_t>(j) * a.kv_dim;
+            for (int d0 = 4 * lane; d0 < hd; d0 += 128) {
+                const uint2 u = *reinterpret_cast<const uint2*>(kj + d0);
+                acc += qs[d0] * __uint_as_float(u.x << 16) + qs[d0 + 1] * __uint_as_float(u.x & 0xFFFF0000u) +
+                       qs[d0 + 2] * __uint_as_float(u.y << 16) + qs[d0 + 3] * __uint_as_float(u.y & 0xFFFF0000u);
             }
         } else {
             const uint16_t* kj = kc + static_cast<size_t>(j) * a.kv_dim;
-            for (int d = 0; d < hd; ++d) acc += qs[d] * bf16_to_f32(kj[d]);
+            for (int d = lane; d < hd; d += 32) acc += qs[d] * bf16_to_f32(kj[d]);
         }
-        scores[j] = acc * inv_sqrt_hd;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) scores[j] = acc * inv_sqrt_hd;
     }
     __syncthreads();
     // softmax (nn_ops.hpp:48-57)
@@ -173,16 +182,40 @@ __global__ void attn_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos
     }
     sum = block_sum(sum, red);
     __syncthreads();
-    // ctx (serve.cpp:276-281): sequential over positions, like the reference;
-    // value rows read coalesced across the threads of the block
+    // ctx (serve.cpp:276-281): p_j = e_j / sum as in the reference; warp w sums the
+    // positions j = w (mod nw) for dims [4l, 4l+4), then the warps' partials are
+    // added in warp order (fixed) through shared memory
+    float* part = scores + a.max_seq;  // [nw][hd]
+    for (int d0 = 4 * lane; d0 < hd; d0 += 128) {
+        float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        for (int j = warp; j < n_ctx; j += nw) {
+            const float pj = scores[j] / sum;
+            float v[4];
+            if (j == pos) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) v[e] = d0 + e < hd ? vs[d0 + e] : 0.0f;
+            } else if (vec) {
+                const uint2 u = *reinterpret_cast<const uint2*>(vc + static_cast<size_t>(j) * a.kv_dim + d0);
+                v[0] = __uint_as_float(u.x << 16);
+                v[1] = __uint_as_float(u.x & 0xFFFF0000u);
+                v[2] = __uint_as_float(u.y << 16);
+                v[3] = __uint_as_float(u.y & 0xFFFF0000u);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    v[e] = d0 + e < hd ? bf16_to_f32(vc[static_cast<size_t>(j) * a.kv_dim + d0 + e]) : 0.0f;
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[e] += pj * v[e];
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (d0 + e < hd) part[warp * hd + d0 + e] = acc[e];
+    }
+    __syncthreads();
     for (int d = threadIdx.x; d < hd; d += blockDim.x) {
         float acc = 0.0f;
-        const uint16_t* vcol = vc + d;
-#pragma unroll 8
-        for (int j = 0; j < n_ctx; ++j) {
-            const float v = (j == pos) ? vs[d] : bf16_to_f32(vcol[static_cast<size_t>(j) * a.kv_dim]);
-            acc += (scores[j] / sum) * v;
-        }
+        for (int w = 0; w < nw; ++w) acc += part[w * hd + d];
         ctx_out[size_t(b) * ld_ctx + h * hd + d] = f32_to_bf16(acc);
     }
 }
@@ -247,13 +280,14 @@ void resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const 
 
 void attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int batch,
                  uint16_t* ctx, int ld_ctx, cudaStream_t s) {
-    const size_t smem = (3 * a.hd + a.max_seq) * sizeof(float);
+    constexpr int kAttnThreads = 256;
+    const size_t smem = (3 * a.hd + a.max_seq + (kAttnThreads / 32) * a.hd) * sizeof(float);
     static bool attr = false;
     if (!attr) {
         BD_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    attn_kernel<<<dim3(a.n_heads, batch), 128, smem, s>>>(qkv, a, pos_dev, ctx, ld_ctx);
+    attn_kernel<<<dim3(a.n_heads, batch), kAttnThreads, smem, s>>>(qkv, a, pos_dev, ctx, ld_ctx);
     note_launch();
     BD_CUDA(cudaGetLastError());
 }

@@ -108,12 +108,11 @@ struct LutJob {
     float alpha[kLutMaxSegs][kMaxPlanesPerUnit];
 };
 struct LutParams {
-    int n_jobs, slices, n_chunks, cols, ldx, batch, M;
-    int seg_row0[kLutMaxSegs];
-    int chunk_seg[kLutMaxChunks], chunk_begin[kLutMaxChunks], chunk_end[kLutMaxChunks];
+    int n_jobs, slices, cols, ldx, batch, M, n_segs, grid;
+    int seg_row0[kLutMaxSegs + 1];  // stacked row offsets of the sub-matrices
     LutJob jobs[kLutMaxJobs];
 };
-// Chunking of the stacked rows (seg_rows) into CTAs; returns false if unsupported.
+// Fills the geometry (slices, persistent grid) for the stacked rows; false if unsupported.
 bool plan_lut(LutParams& p, const int* seg_rows, int n_segs, int cols, int ldx, int batch);
 // out: [slices][batch][M] f32, alpha already applied; every (slice, req, row) of a job written
 void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream);

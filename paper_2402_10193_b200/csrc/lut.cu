@@ -6,15 +6,18 @@
 // reading every plane row with fully coalesced 128-byte warp loads straight from
 // the reference layout (flat row-major bits, LSB first), no re-tiling.
 //
-// A CTA owns (job = one request and its tenant's planes, 1024-column slice,
-// chunk of rows). It first builds, for the slice's x values, 128 byte-tables
-// T[k][e][l] = sum_{i<8} (bit_i(e) ? +x : -x)[32 l + 8 k + i]   (128 KB smem)
-// laid out so that lane l always reads bank l (conflict-free), then for every
-// row each lane loads its 32-bit word of the row slice and adds 4 table
-// entries. 32 rows are accumulated per warp and reduced with a transposing
-// butterfly (31 shuffles per 32 rows). Cost per 8 bits: 2 ALU + 1 LDS + 1 FADD.
-// Output: one f32 partial per (slice, request, row), already scaled by alpha;
-// the consumer kernel sums slices in a fixed order (deterministic).
+// Work = (unit = request x 1024-column slice) x (stacked output rows). The grid
+// is persistent (<= one CTA per SM): CTA c owns a contiguous range of the
+// flattened (unit, row) space, so it rebuilds its tables only when it crosses
+// into a new unit and every SM gets the same amount of work (no wave tail).
+// For a unit the CTA builds 128 byte tables for the slice's x values
+//   T[k][e][l] = sum_{i<8} (bit_i(e) ? +x : -x)[32 l + 8 k + i]   (128 KB smem)
+// laid out so that lane l always reads bank l (conflict-free); then for every
+// row each lane loads its 32-bit word of the row slice and adds 4 entries.
+// 32 rows are accumulated per warp and reduced with a transposing butterfly
+// (31 shuffles per 32 rows). Cost per 8 bits: 2 ALU + 1 LDS + 1 FADD.
+// Output: one f32 partial per (slice, request, row), scaled by alpha; the
+// consumer sums the slices in a fixed order (deterministic).
 #include <algorithm>
 
 #include "common.cuh"
@@ -29,110 +32,122 @@ namespace {
 constexpr int kLutThreads = 512;
 constexpr int kSliceCols = 1024;
 constexpr size_t kTableBytes = 4 * 256 * 32 * sizeof(float);  // 128 KB
+constexpr int R = 32;                                          // rows per warp batch
 
+// Table layout (bytes): entry (k, e, lane l) at (k>>1)*65536 + e*256 + (k&1)*128 + 4*l,
+// so the lookup address of byte k of a word is a single PRMT (byte k of the word
+// placed at bit 8, the lane offset in the low byte) plus an immediate.
+__device__ __forceinline__ void build_tables(float* T, const float* xs) {
+    // thread t -> table (k, l) = t/4, quarter t%4 of its 256 entries; entry = hi nibble + lo nibble
+    const int tb = threadIdx.x >> 2, quarter = threadIdx.x & 3;
+    const int k = tb >> 5, l = tb & 31;
+    const float* xv = xs + 32 * l + 8 * k;
+    float lo[16], hi[4];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        float s = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s += (e >> i & 1) ? xv[i] : -xv[i];
+        lo[e] = s;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int eh = quarter * 4 + e;
+        float s = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s += (eh >> i & 1) ? xv[4 + i] : -xv[4 + i];
+        hi[e] = s;
+    }
+    float* Tk = T + (k >> 1) * 16384 + (k & 1) * 32 + l;  // float index
+#pragma unroll
+    for (int eh = 0; eh < 4; ++eh)
+#pragma unroll
+        for (int el = 0; el < 16; ++el) Tk[((quarter * 4 + eh) * 16 + el) * 64] = hi[eh] + lo[el];
+}
+
+template <int kWPR>  // words per plane row (cols/32); 0 = runtime value
 __global__ void __launch_bounds__(kLutThreads, 1)
     lut_kernel(const __grid_constant__ LutParams p, const uint16_t* __restrict__ X,
                float* __restrict__ out) {
-    extern __shared__ float T[];  // [4][256][32]
+    extern __shared__ float T[];
     __shared__ float xs[kSliceCols];
-    // locate (job, slice, chunk)
-    const int per_job = p.slices * p.n_chunks;
-    const int job_i = blockIdx.x / per_job;
-    const int rem = blockIdx.x % per_job;
-    const int slice = rem / p.n_chunks;
-    const int chunk = rem % p.n_chunks;
-    const LutJob& job = p.jobs[job_i];
-    const int c0 = slice * kSliceCols;
-    // x of this slice (bf16 -> f32), zero past cols
-    const uint16_t* xr = X + static_cast<size_t>(job.req) * p.ldx;
-    for (int i = threadIdx.x; i < kSliceCols; i += kLutThreads)
-        xs[i] = (c0 + i < p.cols) ? bf16_to_f32(xr[c0 + i]) : 0.0f;
-    __syncthreads();
-    // build the 128 tables: thread t -> table (k, l) = t/4, quarter t%4 of its 256 entries
-    {
-        const int tb = threadIdx.x >> 2, quarter = threadIdx.x & 3;
-        const int k = tb >> 5, l = tb & 31;
-        const float* xv = xs + 32 * l + 8 * k;
-        float lo[16], hi[4];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            float s = 0.0f;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) s += (e >> i & 1) ? xv[i] : -xv[i];
-            lo[e] = s;
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int eh = quarter * 4 + e;
-            float s = 0.0f;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) s += (eh >> i & 1) ? xv[4 + i] : -xv[4 + i];
-            hi[e] = s;
-        }
-        float* Tk = T + (k * 256) * 32 + l;
-#pragma unroll
-        for (int eh = 0; eh < 4; ++eh)
-#pragma unroll
-            for (int el = 0; el < 16; ++el) Tk[((quarter * 4 + eh) * 16 + el) * 32] = hi[eh] + lo[el];
-    }
-    __syncthreads();
-
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int seg = p.chunk_seg[chunk];
-    const int r_begin = p.chunk_begin[chunk], r_end = p.chunk_end[chunk];  // rows within seg
-    const int n_planes = job.n_planes[seg];
-    const bool lane_on = c0 + 32 * lane < p.cols;
-    const size_t words_per_row = p.cols / 32;
-    const float* T0 = T + lane;
-    constexpr int R = 16;                       // rows per warp batch
     constexpr int kWarps = kLutThreads / 32;
-    float* outp = out + (static_cast<size_t>(slice) * p.batch + job.req) * p.M + p.seg_row0[seg];
-    for (int pl = 0; pl < n_planes; ++pl) {
-        const uint32_t* bits = reinterpret_cast<const uint32_t*>(job.bits[seg][pl]) + slice * 32 + lane;
-        const float a = job.alpha[seg][pl];
-        auto load = [&](int rb, uint32_t (&w)[R]) {
+    const uint32_t lb0 = 4u * lane, lb1 = 4u * lane + 128u;  // low byte of the entry offset
+    const char* Tc = reinterpret_cast<const char*>(T);
+    const int wpr = kWPR ? kWPR : p.cols / 32;
+    const long long total = static_cast<long long>(p.n_jobs) * p.slices * p.M;
+    const long long g0 = total * blockIdx.x / gridDim.x;
+    const long long g1 = total * (blockIdx.x + 1) / gridDim.x;
+    int cur = -1;
+    for (long long g = g0; g < g1;) {
+        const int u = static_cast<int>(g / p.M);
+        const int ra = static_cast<int>(g % p.M);
+        const int rb = static_cast<int>(std::min<long long>(p.M, ra + (g1 - g)));
+        const int job_i = u / p.slices, slice = u % p.slices;
+        const LutJob& job = p.jobs[job_i];
+        const int c0 = slice * kSliceCols;
+        if (u != cur) {
+            __syncthreads();  // previous unit's lookups done
+            const uint16_t* xr = X + static_cast<size_t>(job.req) * p.ldx;
+            for (int i = threadIdx.x; i < kSliceCols; i += kLutThreads)
+                xs[i] = (c0 + i < p.cols) ? bf16_to_f32(xr[c0 + i]) : 0.0f;
+            __syncthreads();
+            build_tables(T, xs);
+            __syncthreads();
+            cur = u;
+        }
+        const bool lane_on = c0 + 32 * lane < p.cols;
+        float* out_u = out + (static_cast<size_t>(slice) * p.batch + job.req) * p.M;
+        for (int s = 0; s < p.n_segs; ++s) {
+            const int s0 = p.seg_row0[s], s1 = p.seg_row0[s + 1];
+            const int la = std::max(ra, s0) - s0, lb = std::min(rb, s1) - s0;
+            if (la >= lb) continue;
+            for (int r0 = la + warp * R; r0 < lb; r0 += kWarps * R) {
+                float acc[R];
+                const bool full = lane_on && r0 + R <= lb;
+                for (int pl = 0; pl < job.n_planes[s]; ++pl) {
+                    const uint32_t* rowp = reinterpret_cast<const uint32_t*>(job.bits[s][pl]) +
+                                           static_cast<size_t>(r0) * wpr + slice * 32 + lane;
+                    const float a = job.alpha[s][pl];
+                    uint32_t w[R];
+                    if (full) {
 #pragma unroll
-            for (int j = 0; j < R; ++j) {
-                const int r = rb + j;
-                w[j] = (lane_on && r < r_end) ? __ldcs(bits + static_cast<size_t>(r) * words_per_row) : 0u;
-            }
-        };
-        uint32_t wn[R];
-        int rb = r_begin + warp * R;
-        if (rb < r_end) load(rb, wn);
-        for (; rb < r_end; rb += kWarps * R) {
-            uint32_t w[R];
+                        for (int j = 0; j < R; ++j) w[j] = __ldcs(rowp + j * wpr);
+                    } else {
 #pragma unroll
-            for (int j = 0; j < R; ++j) w[j] = wn[j];
-            if (rb + kWarps * R < r_end) load(rb + kWarps * R, wn);  // prefetch next batch
-            float acc[R];
+                        for (int j = 0; j < R; ++j) w[j] = (lane_on && r0 + j < lb) ? __ldcs(rowp + j * wpr) : 0u;
+                    }
 #pragma unroll
-            for (int j = 0; j < R; ++j) {
-                const uint32_t v = w[j];
-                acc[j] = a * (T0[(v & 0xFF) * 32] + T0[(256 + ((v >> 8) & 0xFF)) * 32] +
-                              T0[(512 + ((v >> 16) & 0xFF)) * 32] + T0[(768 + (v >> 24)) * 32]);
-            }
-            // transposing butterfly over lane bits 4..1, then pair-sum: lanes 2i, 2i+1 hold row i
-#pragma unroll
-            for (int o = 16, n = R / 2; o >= 2; o >>= 1, n >>= 1) {
-                const bool upper = (lane & o) != 0;
-#pragma unroll
-                for (int j = 0; j < n; ++j) {
-                    const float send = upper ? acc[j] : acc[j + n];
-                    const float keep = upper ? acc[j + n] : acc[j];
-                    acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                    for (int j = 0; j < R; ++j) {
+                        const uint32_t v = w[j];
+                        const float t0 = *reinterpret_cast<const float*>(Tc + __byte_perm(v, lb0, 0x5504));
+                        const float t1 = *reinterpret_cast<const float*>(Tc + __byte_perm(v, lb1, 0x5514));
+                        const float t2 = *reinterpret_cast<const float*>(Tc + 65536 + __byte_perm(v, lb0, 0x5524));
+                        const float t3 = *reinterpret_cast<const float*>(Tc + 65536 + __byte_perm(v, lb1, 0x5534));
+                        const float sum = (t0 + t1) + (t2 + t3);
+                        acc[j] = pl == 0 ? a * sum : fmaf(a, sum, acc[j]);
+                    }
                 }
-            }
-            const float tot = acc[0] + __shfl_xor_sync(0xffffffffu, acc[0], 1);
-            // row held by lane: bits 4..1 of the lane select 8,4,2,1
-            const int row = rb + ((lane >> 1) & 15);
-            if ((lane & 1) == 0 && row < r_end) {
-                if (pl == 0) outp[row] = tot;
-                else outp[row] += tot;
+                // transposing butterfly: afterwards lane l holds the sum of row r0 + l
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) {
+                    const bool upper = (lane & o) != 0;
+#pragma unroll
+                    for (int j = 0; j < o; ++j) {
+                        const float send = upper ? acc[j] : acc[j + o];
+                        const float keep = upper ? acc[j + o] : acc[j];
+                        acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                    }
+                }
+                const int r = r0 + lane;
+                if (r < lb) out_u[s0 + r] = acc[0];
             }
         }
+        g += rb - ra;
     }
 }
+
 }  // namespace
 
 size_t lut_smem_bytes() { return kTableBytes; }
@@ -148,43 +163,41 @@ bool plan_lut(LutParams& p, const int* seg_rows, int n_segs, int cols, int ldx, 
     p.ldx = ldx;
     p.batch = batch;
     p.slices = (cols + kSliceCols - 1) / kSliceCols;
+    p.n_segs = n_segs;
     int total = 0;
     for (int s = 0; s < n_segs; ++s) {
         p.seg_row0[s] = total;
         total += seg_rows[s];
     }
+    p.seg_row0[n_segs] = total;
     p.M = total;
-    // enough CTAs for ~2 waves at 1 CTA/SM, chunks of >= 512 rows (table build amortised)
-    const int units = p.n_jobs * p.slices;
-    const int want = std::max(1, (2 * kNumSMs + units - 1) / units);
-    int chunk = std::max(512, ((total + want - 1) / want + 31) / 32 * 32);
-    for (;;) {
-        int n = 0;
-        for (int s = 0; s < n_segs; ++s) n += (seg_rows[s] + chunk - 1) / chunk;
-        if (n <= kLutMaxChunks) break;
-        chunk *= 2;
-    }
-    p.n_chunks = 0;
-    for (int s = 0; s < n_segs; ++s)
-        for (int r = 0; r < seg_rows[s]; r += chunk) {
-            p.chunk_seg[p.n_chunks] = s;
-            p.chunk_begin[p.n_chunks] = r;
-            p.chunk_end[p.n_chunks] = std::min(seg_rows[s], r + chunk);
-            ++p.n_chunks;
-        }
+    // persistent: one CTA per SM, but keep >= 512 rows of work per CTA
+    const long long work = static_cast<long long>(p.n_jobs) * p.slices * p.M;
+    p.grid = static_cast<int>(std::max<long long>(1, std::min<long long>(kNumSMs, work / 512)));
     return true;
 }
 
-void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream) {
+template <int kWPR>
+void lut_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t stream) {
     static bool attr = false;
     if (!attr) {
-        BD_CUDA(cudaFuncSetAttribute(lut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        BD_CUDA(cudaFuncSetAttribute(lut_kernel<kWPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(kTableBytes)));
         attr = true;
     }
-    const int grid = p.n_jobs * p.slices * p.n_chunks;
-    if (grid == 0) return;
-    lut_kernel<<<grid, kLutThreads, kTableBytes, stream>>>(p, static_cast<const uint16_t*>(X), out);
+    lut_kernel<kWPR><<<p.grid, kLutThreads, kTableBytes, stream>>>(p, static_cast<const uint16_t*>(X), out);
+}
+
+void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream) {
+    // compile-time row strides for the published shapes (immediate load offsets)
+    switch (p.cols) {
+        case 4096: lut_launch_t<128>(p, X, out, stream); break;
+        case 8192: lut_launch_t<256>(p, X, out, stream); break;
+        case 11008: lut_launch_t<344>(p, X, out, stream); break;
+        case 14336: lut_launch_t<448>(p, X, out, stream); break;
+        case 28672: lut_launch_t<896>(p, X, out, stream); break;
+        default: lut_launch_t<0>(p, X, out, stream); break;
+    }
     note_launch();
     BD_CUDA(cudaGetLastError());
 }
