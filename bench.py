@@ -181,7 +181,7 @@ def run_ours(args, rank, world, dev):
     arch = dict(wl["arch"], rope_theta=10000.0)
     T = args.tenants or wl["tenants"]
     B = args.batch or wl["batch"]
-    ctx = wl["ctx"]
+    ctx = args.ctx or wl["ctx"]
     arch["max_seq"] = ctx + args.warmup + 2 * args.steps + 8
     torch.manual_seed(rank)
     pool, _, setup_s = build_pool(arch, T, dev, seed=1234 + rank)
@@ -405,6 +405,7 @@ def main():
     ap.add_argument("--workload", default="l7_stack", choices=sorted(WORKLOADS))
     ap.add_argument("--tenants", type=int, default=0)
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--ctx", type=int, default=0, help="context length before timing (default: workload)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

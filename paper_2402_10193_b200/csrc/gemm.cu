@@ -196,7 +196,7 @@ CUtensorMap make_tmap_2d(const void* ptr, CUtensorMapDataType dt, uint32_t elem_
     return m;
 }
 
-GemmPlan plan_base_gemm(uint64_t M, uint64_t K, int batch, int ctas_per_sm_hint) {
+GemmPlan plan_base_gemm(uint64_t M, uint64_t K, int batch, int smem_cap) {
     GemmPlan p;
     p.M = M;
     p.K = K;
@@ -204,13 +204,21 @@ GemmPlan plan_base_gemm(uint64_t M, uint64_t K, int batch, int ctas_per_sm_hint)
     p.bn = std::max(16, ((batch + 15) / 16) * 16);
     require(p.bn <= 256, BD_ERR_BAD_ARGUMENT, "base gemm: batch chunk must be <= 256");
     const GemmSmemLayout L0 = gemm_layout(p.bn, 1);
-    // as many stages as fit in ~200 KB (2 CTAs/SM when the stage is small)
-    int stages = std::min(kMaxStages, int((200 * 1024 - 1024 - 256) / L0.stage_bytes));
-    const bool two_per_sm = (gemm_layout(p.bn, 4).total * 2 <= 227 * 1024);
-    if (two_per_sm) stages = std::min(stages, int((110 * 1024 - 1280) / L0.stage_bytes));
-    p.stages = std::max(2, stages);
+    int slots;
+    if (smem_cap > 0) {
+        // co-resident with another kernel on every SM (the K3 LUT): one CTA per SM
+        // within the shared-memory left over
+        p.stages = std::max(2, std::min(kMaxStages, int((smem_cap - 1280) / L0.stage_bytes)));
+        slots = kNumSMs;
+    } else {
+        // as many stages as fit in ~200 KB (2 CTAs/SM when the stage is small)
+        int stages = std::min(kMaxStages, int((200 * 1024 - 1024 - 256) / L0.stage_bytes));
+        const bool two_per_sm = (gemm_layout(p.bn, 4).total * 2 <= 227 * 1024);
+        if (two_per_sm) stages = std::min(stages, int((110 * 1024 - 1280) / L0.stage_bytes));
+        p.stages = std::max(2, stages);
+        slots = kNumSMs * (two_per_sm ? 2 : 1);
+    }
     p.smem = gemm_layout(p.bn, p.stages).total;
-    const int slots = kNumSMs * (two_per_sm ? 2 : 1) * std::max(1, ctas_per_sm_hint);
     const int m_tiles = int((M + kBM - 1) / kBM);
     const int kb = int((K + kBK - 1) / kBK);
     // split-K to fill the machine: minimise ceil(tiles*s/slots) * ceil(kb/s)

@@ -17,7 +17,8 @@ struct GemmPlan {
     int batch = 0, bn = 16, stages = 4, smem = 0;
     int m_tiles = 0, kb_total = 0, kb_per_split = 0, splits = 1;
 };
-GemmPlan plan_base_gemm(uint64_t M, uint64_t K, int batch, int ctas_per_sm_hint = 1);
+// smem_cap > 0: plan one CTA per SM within smem_cap bytes (co-resident with the K3 LUT)
+GemmPlan plan_base_gemm(uint64_t M, uint64_t K, int batch, int smem_cap = 0);
 CUtensorMap make_tmap_2d(const void* ptr, CUtensorMapDataType dt, uint32_t elem_bytes,
                          uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
                          uint32_t box_rows, uint32_t box_cols, bool swizzle128);

@@ -30,9 +30,11 @@ void note_launch();
 namespace {
 
 constexpr int kLutThreads = 512;
+// <= 96 registers so a base-GEMM CTA (128 threads) can be co-resident on the SM
+constexpr int kLutRegs = 96;
 constexpr int kSliceCols = 1024;
 constexpr size_t kTableBytes = 4 * 256 * 32 * sizeof(float);  // 128 KB
-constexpr int R = 32;                                          // rows per warp batch
+constexpr int R = 16;                                          // rows per warp batch
 
 // Table layout (bytes): entry (k, e, lane l) at (k>>1)*65536 + e*256 + (k&1)*128 + 4*l,
 // so the lookup address of byte k of a word is a single PRMT (byte k of the word
@@ -66,7 +68,7 @@ __device__ __forceinline__ void build_tables(float* T, const float* xs) {
 }
 
 template <int kWPR>  // words per plane row (cols/32); 0 = runtime value
-__global__ void __launch_bounds__(kLutThreads, 1)
+__global__ void __maxnreg__(kLutRegs)
     lut_kernel(const __grid_constant__ LutParams p, const uint16_t* __restrict__ X,
                float* __restrict__ out) {
     extern __shared__ float T[];
@@ -103,21 +105,31 @@ __global__ void __launch_bounds__(kLutThreads, 1)
             const int s0 = p.seg_row0[s], s1 = p.seg_row0[s + 1];
             const int la = std::max(ra, s0) - s0, lb = std::min(rb, s1) - s0;
             if (la >= lb) continue;
-            for (int r0 = la + warp * R; r0 < lb; r0 += kWarps * R) {
-                float acc[R];
-                const bool full = lane_on && r0 + R <= lb;
-                for (int pl = 0; pl < job.n_planes[s]; ++pl) {
-                    const uint32_t* rowp = reinterpret_cast<const uint32_t*>(job.bits[s][pl]) +
-                                           static_cast<size_t>(r0) * wpr + slice * 32 + lane;
-                    const float a = job.alpha[s][pl];
-                    uint32_t w[R];
-                    if (full) {
+            const int n_planes = job.n_planes[s];
+            // software pipeline: the words of the warp's next batch are in flight
+            // while the current batch is looked up (one plane at a time)
+            for (int pl = 0; pl < n_planes; ++pl) {
+                const uint32_t* plane = reinterpret_cast<const uint32_t*>(job.bits[s][pl]) + slice * 32 + lane;
+                const float a = job.alpha[s][pl];
+                auto load = [&](int r0, uint32_t (&w)[R]) {
+                    const uint32_t* rowp = plane + static_cast<size_t>(r0) * wpr;
+                    if (lane_on && r0 + R <= lb) {
 #pragma unroll
                         for (int j = 0; j < R; ++j) w[j] = __ldcs(rowp + j * wpr);
                     } else {
 #pragma unroll
                         for (int j = 0; j < R; ++j) w[j] = (lane_on && r0 + j < lb) ? __ldcs(rowp + j * wpr) : 0u;
                     }
+                };
+                uint32_t wn[R];
+                int r0 = la + warp * R;
+                if (r0 < lb) load(r0, wn);
+                for (; r0 < lb; r0 += kWarps * R) {
+                    uint32_t w[R];
+#pragma unroll
+                    for (int j = 0; j < R; ++j) w[j] = wn[j];
+                    if (r0 + kWarps * R < lb) load(r0 + kWarps * R, wn);
+                    float acc[R];
 #pragma unroll
                     for (int j = 0; j < R; ++j) {
                         const uint32_t v = w[j];
@@ -125,23 +137,27 @@ __global__ void __launch_bounds__(kLutThreads, 1)
                         const float t1 = *reinterpret_cast<const float*>(Tc + __byte_perm(v, lb1, 0x5514));
                         const float t2 = *reinterpret_cast<const float*>(Tc + 65536 + __byte_perm(v, lb0, 0x5524));
                         const float t3 = *reinterpret_cast<const float*>(Tc + 65536 + __byte_perm(v, lb1, 0x5534));
-                        const float sum = (t0 + t1) + (t2 + t3);
-                        acc[j] = pl == 0 ? a * sum : fmaf(a, sum, acc[j]);
+                        acc[j] = a * ((t0 + t1) + (t2 + t3));
+                    }
+                    // transposing butterfly over lane bits 4..1, then a pair sum:
+                    // lanes 2i and 2i+1 end with the total of row r0 + i
+#pragma unroll
+                    for (int o = 16, n = R / 2; o >= 2; o >>= 1, n >>= 1) {
+                        const bool upper = (lane & o) != 0;
+#pragma unroll
+                        for (int j = 0; j < n; ++j) {
+                            const float send = upper ? acc[j] : acc[j + n];
+                            const float keep = upper ? acc[j + n] : acc[j];
+                            acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                        }
+                    }
+                    const float tot = acc[0] + __shfl_xor_sync(0xffffffffu, acc[0], 1);
+                    const int r = r0 + ((lane >> 1) & 15);
+                    if ((lane & 1) == 0 && r < lb) {
+                        if (pl == 0) out_u[s0 + r] = tot;
+                        else out_u[s0 + r] += tot;  // same thread wrote it for plane 0
                     }
                 }
-                // transposing butterfly: afterwards lane l holds the sum of row r0 + l
-#pragma unroll
-                for (int o = 16; o >= 1; o >>= 1) {
-                    const bool upper = (lane & o) != 0;
-#pragma unroll
-                    for (int j = 0; j < o; ++j) {
-                        const float send = upper ? acc[j] : acc[j + o];
-                        const float keep = upper ? acc[j + o] : acc[j];
-                        acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-                    }
-                }
-                const int r = r0 + lane;
-                if (r < lb) out_u[s0 + r] = acc[0];
             }
         }
         g += rb - ra;

@@ -171,6 +171,9 @@ struct PoolImpl {
     std::map<std::string, std::unique_ptr<Plan>> plans;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    cudaStream_t stream2 = nullptr;  // side stream: K2 beside K3
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool concurrent_k23 = true;      // BD_SERIAL=1 disables
     bool use_graphs = true;
     bool use_fused = true;
     std::string delta_mode = "auto";  // auto | lut | fused | units (BD_DELTA)
@@ -185,6 +188,9 @@ struct PoolImpl {
         for (void* p : allocs) cudaFree(p);
         if (ev_in) cudaEventDestroy(ev_in);
         if (ev_out) cudaEventDestroy(ev_out);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
+        if (stream2) cudaStreamDestroy(stream2);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -232,6 +238,10 @@ struct PoolImpl {
         ld_inter = round_up(a.intermediate, 8);
         BD_CUDA(cudaSetDevice(device));
         BD_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        BD_CUDA(cudaStreamCreateWithFlags(&stream2, cudaStreamNonBlocking));
+        BD_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+        BD_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+        if (const char* e = std::getenv("BD_SERIAL")) concurrent_k23 = (e[0] == '0');
         BD_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         BD_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
         if (const char* e = std::getenv("BD_NO_GRAPH")) use_graphs = (e[0] == '0');
@@ -935,6 +945,17 @@ struct PoolImpl {
         size_t max_per_tenant = 0;
         for (int t : order) max_per_tenant = std::max(max_per_tenant, by_t[t].size());
         if (delta_mode == "lut" || (delta_mode == "auto" && max_per_tenant <= 4)) plan_lut_groups(*p);
+        if (concurrent_k23 && !p->lut.empty()) {
+            // K2 runs beside the K3 LUT on every SM: one GEMM CTA per SM within the
+            // shared memory the LUT leaves (LUT: 132 KB + 512 threads x 96 regs)
+            GemmPlan* gs[4] = {&p->g_qkv, &p->g_o, &p->g_gu, &p->g_down};
+            for (int gi = 0; gi < 4; ++gi)
+                if (p->lut[0][gi].ok) {
+                    *gs[gi] = plan_base_gemm(gs[gi]->M, gs[gi]->K, B, 88 * 1024);
+                    require(uint64_t(gs[gi]->splits) * B * gs[gi]->M <= P_elems, BD_ERR_CUDA,
+                            "split-K workspace too small");
+                }
+        }
         if (delta_mode == "fused" || delta_mode == "auto") plan_fused_groups(*p, order, by_t);
         auto& slot = plans[key];
         slot = std::move(p);
@@ -998,6 +1019,17 @@ struct PoolImpl {
                 const CUtensorMap& mx, const std::vector<DeltaUnit>& units, const uint16_t* X,
                 int ldx, int cols, int B, cudaStream_t s) {
         if (lut_ok(p, l, group)) {
+            if (concurrent_k23 && !profiling) {
+                // K3 (CUDA cores / LSU) and K2 (TMA + tensor pipe) share every SM:
+                // fork the GEMM onto the side stream, join before the consumer
+                BD_CUDA(cudaEventRecord(ev_fork, s));
+                BD_CUDA(cudaStreamWaitEvent(stream2, ev_fork, 0));
+                lut_launch(p.lut[l][group].prm, X, D, s);
+                base_gemm_launch(g, mw, mx, P, stream2);
+                BD_CUDA(cudaEventRecord(ev_join, stream2));
+                BD_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+                return;
+            }
             prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm_launch(g, mw, mx, P, s); });
             prof(BD_PROF_DELTA_QKV + group, s, [&] { lut_launch(p.lut[l][group].prm, X, D, s); });
             return;
