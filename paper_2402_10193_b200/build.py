@@ -20,7 +20,7 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+FLAGS = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", f"-I{INCLUDE}", f"-I{CSRC}"]
 
 
@@ -72,7 +72,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+    _build_cpp_test(force)
     return LIB
+
+
+def _build_cpp_test(force: bool) -> None:
+    """tests/cpp/test_deltakit_gpu: the deltakit_gpu C++ mirror's parity program."""
+    root = os.path.dirname(HERE)
+    src = os.path.join(root, "tests", "cpp", "test_deltakit_gpu.cpp")
+    out = os.path.join(root, "tests", "cpp", "test_deltakit_gpu")
+    if not os.path.exists(src):
+        return
+    hdr = os.path.join(INCLUDE, "deltakit_gpu", "deltakit_gpu.hpp")
+    if not force and not _stale(out, [src, hdr, LIB]):
+        return
+    cmd = ["g++", "-std=c++20", "-O2", f"-I{INCLUDE}", "-I/usr/local/cuda/include", src, f"-L{HERE}",
+           "-lbitdelta_b200", "-Wl,-rpath,$ORIGIN/../../paper_2402_10193_b200", "-L/usr/local/cuda/lib64",
+           "-lcudart", "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"C++ shim test build failed:\n{r.stderr}")
 
 
 if __name__ == "__main__":

@@ -89,6 +89,10 @@ def main():
         d[f"B{B}_tokens"] = stream
         d[f"B{B}_logits"] = np.stack(logits)  # [steps, B, vocab]
     np.savez_compressed(os.path.join(HERE, "toy_decode.npz"), **d)
+    # raw little-endian copies for the C++ shim test (tests/cpp/test_deltakit_gpu.cpp)
+    base.astype("<f4").tofile(os.path.join(HERE, "toy_base.f32"))
+    d["B4_tokens"].astype("<i4").tofile(os.path.join(HERE, "toy_tokens_B4.i32"))
+    d["B4_logits"].astype("<f4").tofile(os.path.join(HERE, "toy_logits_B4.f32"))
     print("golden fixtures written to", HERE)
 
 

@@ -211,3 +211,18 @@ def test_memory_accounting(cuda, toy):
         pool.decode_step([(r0, 1, pos), (r1, 2, pos)])
     kv = 2 * 2 * 4 * 3 * arch["dim"] * arch["n_layers"]
     assert pool.resident_bytes() == backbone + payload + kv
+
+
+def test_cpp_mirror_program(cuda):
+    """The deltakit_gpu C++ mirror (include/deltakit_gpu) passes its re-hosted reference cases."""
+    import subprocess
+
+    from conftest import ROOT
+
+    exe = os.path.join(ROOT, "tests", "cpp", "test_deltakit_gpu")
+    if not os.path.exists(exe):
+        from paper_2402_10193_b200 import build
+
+        build.build()
+    r = subprocess.run([exe, GOLDEN], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ALL PASSED" in r.stdout, r.stdout + r.stderr
