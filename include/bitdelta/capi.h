@@ -132,6 +132,14 @@ typedef struct bd_arch {
 int bd_pool_create(const bd_arch* arch, int device, int world_size, int rank, bd_pool** out);
 void bd_pool_destroy(bd_pool* pool);
 
+/* Multi-GPU (world_size > 1): every rank holds its row shard; per layer the
+ * pool all-gathers (NCCL over NVLink) the attention context, the o-projection
+ * output, the MLP activation and the down-projection output. Rank 0 creates
+ * the id (bd_nccl_unique_id), the caller broadcasts the 128 bytes, every rank
+ * calls bd_pool_init_comm before registering deltas or decoding. */
+int bd_nccl_unique_id(void* id_out /* 128 bytes */);
+int bd_pool_init_comm(bd_pool* pool, const void* id /* 128 bytes */);
+
 /* Backbone tensor by reference name (arch.cpp:51-69: "embed",
  * "layers.{i}.{attn_q,...,norm2}", "final_norm", "lm_head"), full (unsharded)
  * shape. `data` is host memory unless is_device != 0. */

@@ -20,8 +20,24 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_dir() -> str:
+    """NCCL 2.28 shipped with torch (nvidia-nccl wheel): headers + libnccl.so.2."""
+    import importlib.util
+
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations if spec else []):
+        d = os.path.join(base, "nccl")
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    raise RuntimeError("NCCL headers not found (expected site-packages/nvidia/nccl)")
+
+
+NCCL = _nccl_dir()
 FLAGS = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-         "--expt-relaxed-constexpr", f"-I{INCLUDE}", f"-I{CSRC}"]
+         "--expt-relaxed-constexpr", f"-I{INCLUDE}", f"-I{CSRC}", f"-I{NCCL}/include"]
+LDFLAGS = [f"-L{NCCL}/lib", "-l:libnccl.so.2", f"-Xlinker=-rpath={NCCL}/lib"]
 
 
 def _sources():
@@ -67,8 +83,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
     if force or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda"] if False else \
-              [NVCC, *ARCH, "-shared", "-o", LIB, *objs]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, *LDFLAGS]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -43,6 +43,8 @@ void pool_decode_layers(bd_pool* p, const bd_request* r, uint64_t n, const float
 void pool_stats(const bd_pool* p, bd_pool_stats* out);
 void pool_profile_layers(bd_pool* p, const bd_request* r, uint64_t n, const float* xin,
                          float* xout, double* ms, uint64_t* cnt, void* s);
+void nccl_unique_id(void* out);
+void pool_init_comm(bd_pool* p, const void* id);
 
 template <class F>
 int guarded(F&& f) {
@@ -318,6 +320,18 @@ int bd_pool_create(const bd_arch* arch, int device, int world_size, int rank, bd
 }
 void bd_pool_destroy(bd_pool* pool) {
     if (pool) pool_destroy(pool);
+}
+int bd_nccl_unique_id(void* id_out) {
+    return guarded([&] {
+        require(id_out != nullptr, BD_ERR_BAD_ARGUMENT, "nccl_unique_id: null output");
+        nccl_unique_id(id_out);
+    });
+}
+int bd_pool_init_comm(bd_pool* pool, const void* id) {
+    return guarded([&] {
+        require(pool && id, BD_ERR_BAD_ARGUMENT, "init_comm: null argument");
+        pool_init_comm(pool, id);
+    });
 }
 int bd_pool_set_tensor(bd_pool* pool, const char* name, const void* data, bd_dtype dtype,
                        int is_device, uint64_t rows, uint64_t cols) {

@@ -24,6 +24,10 @@ namespace {
 constexpr int kNormChunk = 256;  // elements per block in the residual/norm kernels
 
 __device__ __forceinline__ float proj_val(const ProjOut& p, int b, int m) {
+    if (p.G) {
+        const int r = m / p.g_cols, i = m - r * p.g_cols;
+        return p.G[(static_cast<size_t>(r) * p.g_batch + b) * p.g_cols + i];
+    }
     float s = 0.0f;
     for (int k = 0; k < p.splits; ++k) s += p.P[static_cast<size_t>(k) * p.pstride + size_t(b) * p.M + m];
     if (p.D)
@@ -262,7 +266,40 @@ __global__ void logits_kernel(ProjOut lm, const float* const* __restrict__ raw_d
     }
 }
 
+__global__ void shard_reduce_kernel(ProjOut p, int batch, int n_l, float* __restrict__ dst) {
+    const size_t n = static_cast<size_t>(batch) * n_l;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        dst[i] = proj_val(p, static_cast<int>(i / n_l), static_cast<int>(i % n_l));
+}
+
+__global__ void gather_transpose_kernel(const uint16_t* __restrict__ src, int world, int batch, int n_l,
+                                        uint16_t* __restrict__ dst, int ld) {
+    const size_t n = static_cast<size_t>(world) * batch * n_l;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const size_t r = i / (static_cast<size_t>(batch) * n_l);
+        const size_t rem = i - r * batch * n_l;
+        const size_t b = rem / n_l, c = rem % n_l;
+        dst[b * ld + r * n_l + c] = src[i];
+    }
+}
+
 }  // namespace
+
+void shard_reduce_launch(const ProjOut& p, int batch, int n_l, float* dst, cudaStream_t s) {
+    const size_t n = static_cast<size_t>(batch) * n_l;
+    shard_reduce_kernel<<<static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 1184)), 256, 0, s>>>(p, batch, n_l, dst);
+    note_launch();
+    BD_CUDA(cudaGetLastError());
+}
+
+void gather_transpose_launch(const uint16_t* src, int world, int batch, int n_l, uint16_t* dst, int ld,
+                             cudaStream_t s) {
+    const size_t n = static_cast<size_t>(world) * batch * n_l;
+    gather_transpose_kernel<<<static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 1184)), 256, 0, s>>>(
+        src, world, batch, n_l, dst, ld);
+    note_launch();
+    BD_CUDA(cudaGetLastError());
+}
 
 int norm_chunks(int dim) { return (dim + kNormChunk - 1) / kNormChunk; }
 

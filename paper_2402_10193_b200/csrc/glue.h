@@ -17,7 +17,16 @@ struct ProjOut {
     size_t dstride = 0;
     int M = 0;
     int col0 = 0;  // column offset used by resid_norm (o / down outputs)
+    // all-gathered row shards (world > 1): value(b, m) = G[(m / g_cols) * g_batch + b][m % g_cols]
+    const float* G = nullptr;
+    int g_cols = 0, g_batch = 0;
 };
+
+// [world][batch][n_l] f32 partial sums of a row-sharded projection -> dst [batch][n_l]
+void shard_reduce_launch(const ProjOut& p, int batch, int n_l, float* dst, cudaStream_t s);
+// all-gathered [world][batch][n_l] bf16 -> [batch][ld] (columns r*n_l + i)
+void gather_transpose_launch(const uint16_t* src, int world, int batch, int n_l, uint16_t* dst, int ld,
+                             cudaStream_t s);
 
 struct AttnArgs {
     int dim, kv_dim, n_heads, n_kv_heads, hd, max_seq, layer;

@@ -32,6 +32,14 @@
 #include "glue.h"
 #include "kernels.h"
 
+#include <nccl.h>
+
+#define BD_NCCL(x)                                                                            \
+    do {                                                                                      \
+        const ncclResult_t r_ = (x);                                                          \
+        if (r_ != ncclSuccess) ::bd::fail(BD_ERR_CUDA, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
 namespace bd {
 
 void note_launch();
@@ -164,6 +172,10 @@ struct PoolImpl {
     int ws_B = 0;
     float *x = nullptr, *xn_f32 = nullptr, *P = nullptr, *D = nullptr, *logits = nullptr;
     double* msq = nullptr;  // per-request chunk sums of squares (RMSNorm)
+    // tensor parallel (world > 1)
+    ncclComm_t comm = nullptr;
+    uint16_t *ctx_loc = nullptr, *act_loc = nullptr, *gath16 = nullptr;
+    float *red_loc = nullptr, *gath32 = nullptr;
     uint16_t *xn = nullptr, *ctx = nullptr, *act = nullptr;
     size_t P_elems = 0, D_elems = 0;
     std::vector<void*> ws_allocs;
@@ -191,6 +203,7 @@ struct PoolImpl {
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
         if (stream2) cudaStreamDestroy(stream2);
+        if (comm) ncclCommDestroy(comm);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -667,6 +680,13 @@ struct PoolImpl {
         P = dmalloc<float>(P_elems, &ws_allocs);
         logits = dmalloc<float>(ws_B * a.vocab, &ws_allocs);
         msq = dmalloc<double>(size_t(ws_B) * norm_chunks(int(a.dim)), &ws_allocs);
+        if (world > 1) {
+            ctx_loc = dmalloc<uint16_t>(size_t(ws_B) * q_l, &ws_allocs);
+            act_loc = dmalloc<uint16_t>(size_t(ws_B) * inter_l, &ws_allocs);
+            gath16 = dmalloc<uint16_t>(size_t(world) * ws_B * std::max(q_l, inter_l), &ws_allocs);
+            red_loc = dmalloc<float>(size_t(ws_B) * dim_l, &ws_allocs);
+            gath32 = dmalloc<float>(size_t(world) * ws_B * dim_l, &ws_allocs);
+        }
     }
 
     // Byte-LUT delta path (lut.cu): one job per request, planes read in the
@@ -1050,15 +1070,35 @@ struct PoolImpl {
 
     // the layer loop of decode_shared (serve.cpp:240-310); x holds the
     // residual stream entering layer 0 and leaves it after the last layer
+    // ---- tensor-parallel exchanges (world > 1): NCCL all-gather over NVLink ----
+    // bf16 activation slice [B x n_l] -> every rank's slices -> [B x ld] in column order
+    void exchange_bf16(const uint16_t* local, int B, int n_l, uint16_t* full, int ld, cudaStream_t s) {
+        const size_t cnt = size_t(B) * n_l;
+        BD_NCCL(ncclAllGather(local, gath16, cnt, ncclBfloat16, comm, s));
+        gather_transpose_launch(gath16, world, B, n_l, full, ld, s);
+    }
+    // row-sharded f32 projection output -> gathered view consumed by the residual kernel
+    ProjOut exchange_f32(const ProjOut& part, int B, int n_l, cudaStream_t s) {
+        shard_reduce_launch(part, B, n_l, red_loc, s);
+        BD_NCCL(ncclAllGather(red_loc, gath32, size_t(B) * n_l, ncclFloat32, comm, s));
+        ProjOut g;
+        g.G = gath32;
+        g.g_cols = n_l;
+        g.g_batch = B;
+        return g;
+    }
+
     void run_layers(Plan& p, cudaStream_t s) {
         const int B = p.B;
         const uint64_t nL = a.n_layers;
-        AttnArgs aa{int(a.dim), int(a.kv_dim), int(a.n_heads), int(n_kv_heads), int(hd),
+        const bool tp = world > 1;
+        // attention runs on this rank's heads only (q/k/v are sharded by heads)
+        AttnArgs aa{int(q_l), int(kv_l), int(a.n_heads / world), int(n_kv_heads / world), int(hd),
                     int(a.max_seq), 0, p.d_kc, p.d_vc, rope};
         ProjOut prev;  // pending residual contribution (previous layer's down)
         for (uint64_t l = 0; l < nL; ++l) {
             const LayerW& W = L[l];
-            // x += down(prev); xn = norm1(x)
+            // x += down(prev); xn = norm1(x)   (x and xn replicated on every rank)
             prof(BD_PROF_NORM, s, [&] {
                 resid_norm_launch(x, B, int(a.dim), prev, p.d_norm + (2 * l) * B, xn, int(ld_dim),
                                   nullptr, msq, s);
@@ -1066,20 +1106,27 @@ struct PoolImpl {
             linear(p, l, 0, p.g_qkv, W.m_qkv, p.x_xn, p.units[l][0], xn, int(ld_dim), int(a.dim), B, s);
             aa.layer = int(l);
             prof(BD_PROF_ATTN, s, [&] {
-                attn_launch(group_out(p, l, 0, p.g_qkv), aa, p.d_pos, B, ctx, int(ld_dim), s);
+                attn_launch(group_out(p, l, 0, p.g_qkv), aa, p.d_pos, B, tp ? ctx_loc : ctx,
+                            tp ? int(q_l) : int(ld_dim), s);
             });
+            if (tp) exchange_bf16(ctx_loc, B, int(q_l), ctx, int(ld_dim), s);
             linear(p, l, 1, p.g_o, W.m_o, p.x_ctx, p.units[l][1], ctx, int(ld_dim), int(a.dim), B, s);
+            const ProjOut o_out = tp ? exchange_f32(group_out(p, l, 1, p.g_o), B, int(dim_l), s)
+                                     : group_out(p, l, 1, p.g_o);
             prof(BD_PROF_NORM, s, [&] {
-                resid_norm_launch(x, B, int(a.dim), group_out(p, l, 1, p.g_o),
-                                  p.d_norm + (2 * l + 1) * B, xn, int(ld_dim), nullptr, msq, s);
+                resid_norm_launch(x, B, int(a.dim), o_out, p.d_norm + (2 * l + 1) * B, xn, int(ld_dim),
+                                  nullptr, msq, s);
             });
             linear(p, l, 2, p.g_gu, W.m_gu, p.x_xn, p.units[l][2], xn, int(ld_dim), int(a.dim), B, s);
             prof(BD_PROF_SILU, s, [&] {
-                silu_launch(group_out(p, l, 2, p.g_gu), B, int(a.intermediate), act, int(ld_inter), s);
+                silu_launch(group_out(p, l, 2, p.g_gu), B, int(inter_l), tp ? act_loc : act,
+                            tp ? int(inter_l) : int(ld_inter), s);
             });
+            if (tp) exchange_bf16(act_loc, B, int(inter_l), act, int(ld_inter), s);
             linear(p, l, 3, p.g_down, W.m_down, p.x_act, p.units[l][3], act, int(ld_inter),
                    int(a.intermediate), B, s);
-            prev = group_out(p, l, 3, p.g_down);
+            prev = tp ? exchange_f32(group_out(p, l, 3, p.g_down), B, int(dim_l), s)
+                      : group_out(p, l, 3, p.g_down);
         }
         prof(BD_PROF_NORM, s, [&] {
             resid_norm_launch(x, B, int(a.dim), prev, nullptr, nullptr, 0, nullptr, msq, s);
@@ -1150,6 +1197,8 @@ struct PoolImpl {
         validate(reqs, n);
         if (n == 0) return;
         require(n <= 256, BD_ERR_BAD_ARGUMENT, "decode: batch must be <= 256");
+        require(world == 1 || comm != nullptr, BD_ERR_BAD_ARGUMENT,
+                "decode: world_size > 1 needs bd_pool_init_comm first");
         std::vector<int> idx(n);
         for (uint64_t i = 0; i < n; ++i) {
             idx[i] = int(reqs[i].request_id);
@@ -1285,6 +1334,20 @@ void pool_profile_layers(bd_pool* p, const bd_request* r, uint64_t n, const floa
         cudaEventDestroy(ev.second.second);
     }
     P.prof_events.clear();
+}
+void nccl_unique_id(void* out) {
+    ncclUniqueId id;
+    BD_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
+}
+void pool_init_comm(bd_pool* p, const void* idp) {
+    PoolImpl& P = p->impl;
+    require(P.world > 1, BD_ERR_BAD_ARGUMENT, "init_comm: pool was created with world_size 1");
+    require(P.comm == nullptr, BD_ERR_BAD_ARGUMENT, "init_comm: communicator already initialised");
+    ncclUniqueId id;
+    std::memcpy(&id, idp, sizeof(id));
+    BD_CUDA(cudaSetDevice(P.device));
+    BD_NCCL(ncclCommInitRank(&P.comm, P.world, id, P.rank));
 }
 void pool_stats(const bd_pool* p, bd_pool_stats* out) {
     *out = p->impl.stats;

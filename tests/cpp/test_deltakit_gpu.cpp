@@ -100,7 +100,8 @@ int main(int argc, char** argv) {
         const DenseMatrix m = gaussian(6, 5, 3);
         const PackedSignMatrix p = compress_tensor(m, m);
         CHECK(p.scale == 0.0f);
-        for (float v : decompress_tensor(p).values()) CHECK(v == 0.0f);
+        const DenseMatrix rec = decompress_tensor(p);
+        for (float v : rec.values()) CHECK(v == 0.0f);
     });
     run("bit layout: row-major, LSB-first, zero trailing bits", [] {
         const PackedSignMatrix p = compress_delta(DenseMatrix(3, 3, {1, -1, 1, 1, -1, -1, 1, -1, 1}));
