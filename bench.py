@@ -121,14 +121,20 @@ def kv_bytes(arch, batch, ctx):
 
 
 # --------------------------------------------------------------------- ours --
-def build_pool(arch, n_tenants, dev, seed=0):
+def build_pool(arch, n_tenants, dev, seed=0, world=1, rank=0):
     import torch
 
     import paper_2402_10193_b200 as bd
     from paper_2402_10193_b200.serving import ServingPool, tensor_shapes
 
     g = torch.Generator(device=dev).manual_seed(seed)
-    pool = ServingPool(arch, None, device=dev.index or 0)
+    pool = ServingPool(arch, None, device=dev.index or 0, world_size=world, rank=rank)
+    if world > 1:  # row-sharded pool: rank 0's NCCL id to every rank
+        import torch.distributed as dist
+
+        obj = [ServingPool.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        pool.init_comm(obj[0])
     base = {}
     for name, r, c in tensor_shapes(arch):
         if "norm" in name:
@@ -183,8 +189,11 @@ def run_ours(args, rank, world, dev):
     B = args.batch or wl["batch"]
     ctx = args.ctx or wl["ctx"]
     arch["max_seq"] = ctx + args.warmup + 2 * args.steps + 8
-    torch.manual_seed(rank)
-    pool, _, setup_s = build_pool(arch, T, dev, seed=1234 + rank)
+    tp = args.parallelism == "tp" and world > 1
+    torch.manual_seed(0 if tp else rank)  # tp ranks must see the same activations
+    # replicas: every rank its own pool and batch; tp: one row-sharded pool, same seed everywhere
+    pool, _, setup_s = build_pool(arch, T, dev, seed=1234 if tp else 1234 + rank,
+                                  world=world if tp else 1, rank=rank if tp else 0)
     rids = [pool.open_request(f"tenant{b % T}") for b in range(B)]
     pos = [0] * B
     x = torch.randn(B, arch["dim"], device=dev)
@@ -245,8 +254,9 @@ def run_ours(args, rank, world, dev):
         pos[b] += 1
 
     ms_step = ms_max / args.steps
-    tok_s = world * B / (ms_step / 1e3)
-    return dict(ms_step=ms_step, tok_s=tok_s, e2e_ms=e2e_ms, e2e_tok_s=world * B / (e2e_ms / 1e3),
+    streams = 1 if tp else world  # independent batches in flight across the job
+    tok_s = streams * B / (ms_step / 1e3)
+    return dict(ms_step=ms_step, tok_s=tok_s, e2e_ms=e2e_ms, e2e_tok_s=streams * B / (e2e_ms / 1e3),
                 clocks=clk.summary(), kernels_per_step=kernels_per_step, prof=prof, arch=arch, T=T,
                 B=B, ctx=ctx, setup_s=setup_s, launches=bd.launch_count() - launches0,
                 h2d=B * arch["dim"] * 4, d2h=B * arch["dim"] * 4)
@@ -373,7 +383,9 @@ def run_reference(args):
 def config_of(args, arch, T, B, ctx):
     return {"workload": args.workload, "model": "llama2-7b-shaped" if arch["kv_dim"] == arch["dim"] else
             "mistral-7b-shaped", "layers": arch["n_layers"], "tenants": T, "global_batch": B * args.gpus,
-            "batch_per_gpu": B, "seq_len": ctx, "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single",
+            "batch_per_gpu": B, "seq_len": ctx,
+            "parallelism": (f"tp{args.gpus}" if args.parallelism == "tp" else f"replicas{args.gpus}")
+            if args.gpus > 1 else "single",
             "l2": "working set > L2 (no flush needed)"}
 
 
@@ -406,6 +418,8 @@ def main():
     ap.add_argument("--tenants", type=int, default=0)
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--ctx", type=int, default=0, help="context length before timing (default: workload)")
+    ap.add_argument("--parallelism", default="replicas", choices=["replicas", "tp"],
+                    help="N>1: independent replicas (weak scaling) or one row-sharded pool over NCCL")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -431,7 +445,9 @@ def main():
     byts = algorithmic_bytes(res["arch"], res["T"], res["B"])
     line = {"metric": METRIC, "value": round(res["tok_s"], 2), "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms_step"], 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True,
+            "scaling": "strong" if (args.parallelism == "tp" and world > 1) else "weak",
+            "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (random bf16 backbone; fine = base + N(0,1e-3) compressed on device by K1)",
             "config": config_of(args, res["arch"], res["T"], res["B"], res["ctx"]),
             "e2e": {"value": round(res["e2e_tok_s"], 2), "unit": "tokens/s", "h2d_bytes_per_step": res["h2d"],

@@ -64,7 +64,8 @@ SYMBOLS = [
     "bd_packed_matvec", "bd_multitenant_linear", "bd_pool_create", "bd_pool_destroy",
     "bd_pool_set_tensor", "bd_pool_register_delta", "bd_pool_register_delta_file",
     "bd_pool_open_request", "bd_pool_close_request", "bd_pool_decode_step",
-    "bd_pool_decode_layers", "bd_pool_get_stats", "bd_pool_profile_layers",
+    "bd_pool_decode_layers", "bd_pool_get_stats", "bd_pool_profile_layers", "bd_nccl_unique_id",
+    "bd_pool_init_comm",
 ]
 
 
@@ -99,6 +100,8 @@ def lib() -> C.CDLL:
     L.bd_pool_get_stats.argtypes = [vp, C.POINTER(PoolStats)]
     L.bd_pool_profile_layers.argtypes = [vp, C.POINTER(Request), u64, vp, vp, C.POINTER(C.c_double),
                                          C.POINTER(u64), vp]
+    L.bd_nccl_unique_id.argtypes = [vp]
+    L.bd_pool_init_comm.argtypes = [vp, vp]
     return L
 
 

@@ -57,6 +57,18 @@ class ServingPool:
     def close(self):
         self.__del__()
 
+    # ---- multi-GPU (row-sharded pool, world_size > 1) ----
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().bd_nccl_unique_id(buf))
+        return buf.raw
+
+    def init_comm(self, uid: bytes) -> None:
+        """Every rank, after rank 0's nccl_unique_id() was broadcast."""
+        buf = C.create_string_buffer(uid, 128)
+        check(lib().bd_pool_init_comm(self._h, buf))
+
     # ---- backbone ----
     def set_tensor(self, name: str, data) -> None:
         import torch
