@@ -11,6 +11,7 @@
 // fixed order (no atomics): outputs are bit-reproducible and independent of a
 // request's position in the batch.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "glue.h"
@@ -100,6 +101,49 @@ __global__ void __launch_bounds__(kNormChunk)
     if (xn_f32) xn_f32[size_t(b) * dim + i] = y;
 }
 
+// single-kernel variant: one 1024-thread block per request does the residual add,
+// the double sum of squares (fixed tree) and the normalisation
+constexpr int kFusedNormThreads = 1024;
+__global__ void __launch_bounds__(kFusedNormThreads)
+    resid_norm_one_kernel(float* __restrict__ x, int dim, ProjOut proj, const float* const* __restrict__ norm_w,
+                          uint16_t* __restrict__ xn, int ldxn, float* __restrict__ xn_f32) {
+    __shared__ double red_d[32];
+    const int b = blockIdx.x;
+    float* xb = x + size_t(b) * dim;
+    constexpr int kMaxPer = 16;
+    float v[kMaxPer];
+    double sq = 0.0;
+#pragma unroll
+    for (int k = 0; k < kMaxPer; ++k) {
+        const int i = threadIdx.x + k * kFusedNormThreads;
+        if (i < dim) {
+            float t = xb[i];
+            if (proj.P || proj.G) t = t + proj_val(proj, b, proj.col0 + i);
+            v[k] = t;
+            sq += static_cast<double>(t) * t;
+        }
+    }
+    if (proj.P || proj.G)
+#pragma unroll
+        for (int k = 0; k < kMaxPer; ++k) {
+            const int i = threadIdx.x + k * kFusedNormThreads;
+            if (i < dim) xb[i] = v[k];
+        }
+    if (!norm_w) return;
+    sq = block_sum(sq, red_d);
+    const double inv = 1.0 / sqrt(sq / static_cast<double>(dim) + 1e-12);
+    const float* w = norm_w[b];
+#pragma unroll
+    for (int k = 0; k < kMaxPer; ++k) {
+        const int i = threadIdx.x + k * kFusedNormThreads;
+        if (i < dim) {
+            const float y = static_cast<float>(static_cast<double>(v[k]) * inv) * w[i];
+            if (xn) xn[size_t(b) * ldxn + i] = f32_to_bf16(y);
+            if (xn_f32) xn_f32[size_t(b) * dim + i] = y;
+        }
+    }
+}
+
 // one block per (head, request): RoPE, KV append, scores, softmax, context
 __global__ void attn_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos_dev,
                             uint16_t* __restrict__ ctx_out, int ld_ctx) {
@@ -154,6 +198,33 @@ __global__ void attn_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos
     const float inv_sqrt_hd = 1.0f / sqrtf(static_cast<float>(hd));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const bool vec = (hd % 4) == 0 && (a.kv_dim % 4) == 0;
+    if (vec && hd == 128) {
+        // fast path: 8 keys per warp in flight (all loads issued before the math)
+        const float q0 = qs[4 * lane], q1 = qs[4 * lane + 1], q2 = qs[4 * lane + 2], q3 = qs[4 * lane + 3];
+        for (int j0 = warp; j0 < n_ctx; j0 += nw * 8) {
+            uint2 u[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const int j = j0 + t * nw;
+                u[t] = (j < n_ctx && j != pos)
+                           ? *reinterpret_cast<const uint2*>(kc + static_cast<size_t>(j) * a.kv_dim + 4 * lane)
+                           : make_uint2(0u, 0u);
+            }
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const int j = j0 + t * nw;
+                float acc;
+                if (j == pos)
+                    acc = q0 * ks[4 * lane] + q1 * ks[4 * lane + 1] + q2 * ks[4 * lane + 2] + q3 * ks[4 * lane + 3];
+                else
+                    acc = q0 * __uint_as_float(u[t].x << 16) + q1 * __uint_as_float(u[t].x & 0xFFFF0000u) +
+                          q2 * __uint_as_float(u[t].y << 16) + q3 * __uint_as_float(u[t].y & 0xFFFF0000u);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (lane == 0 && j < n_ctx) scores[j] = acc * inv_sqrt_hd;
+            }
+        }
+    } else
     for (int j = warp; j < n_ctx; j += nw) {
         float acc = 0.0f;
         if (j == pos) {
@@ -190,6 +261,40 @@ __global__ void attn_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos
     // positions j = w (mod nw) for dims [4l, 4l+4), then the warps' partials are
     // added in warp order (fixed) through shared memory
     float* part = scores + a.max_seq;  // [nw][hd]
+    if (vec && hd == 128) {
+        // fast path: 8 value rows per warp in flight
+        float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        for (int j0 = warp; j0 < n_ctx; j0 += nw * 8) {
+            uint2 u[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const int j = j0 + t * nw;
+                u[t] = (j < n_ctx && j != pos)
+                           ? *reinterpret_cast<const uint2*>(vc + static_cast<size_t>(j) * a.kv_dim + 4 * lane)
+                           : make_uint2(0u, 0u);
+            }
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const int j = j0 + t * nw;
+                if (j >= n_ctx) break;
+                const float pj = scores[j] / sum;
+                float v[4];
+                if (j == pos) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) v[e] = vs[4 * lane + e];
+                } else {
+                    v[0] = __uint_as_float(u[t].x << 16);
+                    v[1] = __uint_as_float(u[t].x & 0xFFFF0000u);
+                    v[2] = __uint_as_float(u[t].y << 16);
+                    v[3] = __uint_as_float(u[t].y & 0xFFFF0000u);
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) acc[e] += pj * v[e];
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) part[warp * hd + 4 * lane + e] = acc[e];
+    } else
     for (int d0 = 4 * lane; d0 < hd; d0 += 128) {
         float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
         for (int j = warp; j < n_ctx; j += nw) {
@@ -305,6 +410,15 @@ int norm_chunks(int dim) { return (dim + kNormChunk - 1) / kNormChunk; }
 
 void resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const float* const* norm_w,
                        uint16_t* xn, int ldxn, float* xn_f32, double* msq_ws, cudaStream_t s) {
+    // One-launch variant (16 CTAs) measured slower than the two-phase, 16x wider
+    // grid at batch 16 (1.22 vs 0.73 ms/step); kept for BD_NORM_ONE=1 experiments.
+    static const bool one = std::getenv("BD_NORM_ONE") && std::getenv("BD_NORM_ONE")[0] == '1';
+    if (one && dim <= 16 * kFusedNormThreads) {
+        resid_norm_one_kernel<<<batch, kFusedNormThreads, 0, s>>>(x, dim, proj, norm_w, xn, ldxn, xn_f32);
+        note_launch();
+        BD_CUDA(cudaGetLastError());
+        return;
+    }
     const dim3 grid(norm_chunks(dim), batch);
     resid_kernel<<<grid, kNormChunk, 0, s>>>(x, dim, proj, norm_w ? msq_ws : nullptr);
     note_launch();

@@ -1003,12 +1003,13 @@ struct PoolImpl {
             f();
             return;
         }
+        // external event-record nodes when captured: the graph is timed as it replays
         cudaEvent_t e0, e1;
         BD_CUDA(cudaEventCreate(&e0));
         BD_CUDA(cudaEventCreate(&e1));
-        BD_CUDA(cudaEventRecord(e0, s));
+        BD_CUDA(cudaEventRecordWithFlags(e0, s, cudaEventRecordExternal));
         f();
-        BD_CUDA(cudaEventRecord(e1, s));
+        BD_CUDA(cudaEventRecordWithFlags(e1, s, cudaEventRecordExternal));
         prof_events.push_back({kind, {e0, e1}});
     }
 
@@ -1039,15 +1040,18 @@ struct PoolImpl {
                 const CUtensorMap& mx, const std::vector<DeltaUnit>& units, const uint16_t* X,
                 int ldx, int cols, int B, cudaStream_t s) {
         if (lut_ok(p, l, group)) {
-            if (concurrent_k23 && !profiling) {
+            if (concurrent_k23) {
                 // K3 (CUDA cores / LSU) and K2 (TMA + tensor pipe) share every SM:
-                // fork the GEMM onto the side stream, join before the consumer
-                BD_CUDA(cudaEventRecord(ev_fork, s));
-                BD_CUDA(cudaStreamWaitEvent(stream2, ev_fork, 0));
-                lut_launch(p.lut[l][group].prm, X, D, s);
-                base_gemm_launch(g, mw, mx, P, stream2);
-                BD_CUDA(cudaEventRecord(ev_join, stream2));
-                BD_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+                // fork the GEMM onto the side stream, join before the consumer.
+                // Profiled as one unit (kind FUSED_*: all of K2+K3 for the group).
+                prof(BD_PROF_FUSED_QKV + group, s, [&] {
+                    BD_CUDA(cudaEventRecord(ev_fork, s));
+                    BD_CUDA(cudaStreamWaitEvent(stream2, ev_fork, 0));
+                    lut_launch(p.lut[l][group].prm, X, D, s);
+                    base_gemm_launch(g, mw, mx, P, stream2);
+                    BD_CUDA(cudaEventRecord(ev_join, stream2));
+                    BD_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+                });
                 return;
             }
             prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm_launch(g, mw, mx, P, s); });
@@ -1149,10 +1153,30 @@ struct PoolImpl {
     void execute(Plan& p, bool full) {
         cudaGraphExec_t& g = full ? p.graph_full : p.graph_layers;
         uint64_t& kcount = full ? p.kernels_full : p.kernels_layers;
-        if (!use_graphs || profiling) {
+        if (!use_graphs) {
             const uint64_t c0 = launch_count();
             if (full) run_full(p, stream); else run_layers(p, stream);
             stats.kernels_last_step = launch_count() - c0;
+            return;
+        }
+        if (profiling) {
+            // a throw-away graph with external event-record nodes around every kernel
+            // (or concurrent K2||K3 pair), replayed once: device times as in production
+            cudaGraph_t graph;
+            cudaGraphExec_t ge;
+            BD_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+            try {
+                if (full) run_full(p, stream); else run_layers(p, stream);
+            } catch (...) {
+                cudaStreamEndCapture(stream, &graph);
+                throw;
+            }
+            BD_CUDA(cudaStreamEndCapture(stream, &graph));
+            BD_CUDA(cudaGraphInstantiate(&ge, graph, 0));
+            BD_CUDA(cudaGraphLaunch(ge, stream));
+            BD_CUDA(cudaStreamSynchronize(stream));
+            BD_CUDA(cudaGraphExecDestroy(ge));
+            BD_CUDA(cudaGraphDestroy(graph));
             return;
         }
         if (!g) {
