@@ -110,6 +110,7 @@ struct LutJob {
 };
 struct LutParams {
     int n_jobs, slices, cols, ldx, batch, M, n_segs, grid;
+    int debug;  // experiment flags (BD_LUT_DEBUG), 0 in production
     int seg_row0[kLutMaxSegs + 1];  // stacked row offsets of the sub-matrices
     LutJob jobs[kLutMaxJobs];
 };

@@ -19,6 +19,7 @@
 // Output: one f32 partial per (slice, request, row), scaled by alpha; the
 // consumer sums the slices in a fixed order (deterministic).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -40,10 +41,11 @@ constexpr int R = 16;                                          // rows per warp 
 // so the lookup address of byte k of a word is a single PRMT (byte k of the word
 // placed at bit 8, the lane offset in the low byte) plus an immediate.
 __device__ __forceinline__ void build_tables(float* T, const float* xs) {
-    // thread t -> table (k, l) = t/4, quarter t%4 of its 256 entries; entry = hi nibble + lo nibble
-    const int tb = threadIdx.x >> 2, quarter = threadIdx.x & 3;
-    const int k = tb >> 5, l = tb & 31;
-    const float* xv = xs + 32 * l + 8 * k;
+    // thread t -> lane l = t%32, quarter (t/32)%4 of the 256 entries, table k = t/128;
+    // a warp covers the 32 lanes of one (k, quarter) -> its stores hit 32 distinct banks.
+    // xs is [32][33] (padded) so the per-lane x reads are conflict-free too.
+    const int l = threadIdx.x & 31, quarter = (threadIdx.x >> 5) & 3, k = threadIdx.x >> 7;
+    const float* xv = xs + 33 * l + 8 * k;
     float lo[16], hi[4];
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
@@ -72,7 +74,7 @@ __global__ void __maxnreg__(kLutRegs)
     lut_kernel(const __grid_constant__ LutParams p, const uint16_t* __restrict__ X,
                float* __restrict__ out) {
     extern __shared__ float T[];
-    __shared__ float xs[kSliceCols];
+    __shared__ float xs[32 * 33];  // x of the slice, [lane][32 columns] padded to 33
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int kWarps = kLutThreads / 32;
     const uint32_t lb0 = 4u * lane, lb1 = 4u * lane + 128u;  // low byte of the entry offset
@@ -93,9 +95,9 @@ __global__ void __maxnreg__(kLutRegs)
             __syncthreads();  // previous unit's lookups done
             const uint16_t* xr = X + static_cast<size_t>(job.req) * p.ldx;
             for (int i = threadIdx.x; i < kSliceCols; i += kLutThreads)
-                xs[i] = (c0 + i < p.cols) ? bf16_to_f32(xr[c0 + i]) : 0.0f;
+                xs[(i >> 5) * 33 + (i & 31)] = (c0 + i < p.cols) ? bf16_to_f32(xr[c0 + i]) : 0.0f;
             __syncthreads();
-            build_tables(T, xs);
+            if (!(p.debug & 1)) build_tables(T, xs);
             __syncthreads();
             cur = u;
         }
@@ -190,6 +192,7 @@ bool plan_lut(LutParams& p, const int* seg_rows, int n_segs, int cols, int ldx, 
     // persistent: one CTA per SM, but keep >= 512 rows of work per CTA
     const long long work = static_cast<long long>(p.n_jobs) * p.slices * p.M;
     p.grid = static_cast<int>(std::max<long long>(1, std::min<long long>(kNumSMs, work / 512)));
+    p.debug = std::getenv("BD_LUT_DEBUG") ? std::atoi(std::getenv("BD_LUT_DEBUG")) : 0;
     return true;
 }
 
