@@ -14,6 +14,7 @@
 //
 // Roofline: HBM — 2 bytes per weight element; at batch B the intensity is B
 // flop/byte, far below the tensor pipe's ridge point.
+#include <cstdlib>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -247,6 +248,10 @@ void base_gemm_launch(const GemmPlan& p, const CUtensorMap& map_w, const CUtenso
     if (!attr_set) {
         BD_CUDA(cudaFuncSetAttribute(base_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      227 * 1024));
+        // full carveout: an SM first configured for the co-resident K3 LUT must still
+        // have room for a GEMM CTA (the default picks the smallest fitting carveout)
+        BD_CUDA(cudaFuncSetAttribute(base_gemm_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     int(cudaSharedmemCarveoutMaxShared)));
         attr_set = true;
     }
     dim3 grid(p.m_tiles, p.splits);

@@ -24,15 +24,30 @@ namespace {
 
 constexpr int kNormChunk = 256;  // elements per block in the residual/norm kernels
 
+// k-th partial of output (b, m): base split-K partials first, then delta partials
+__device__ __forceinline__ const float* proj_ptr(const ProjOut& p, int k, int b, int m) {
+    return k < p.splits ? p.P + static_cast<size_t>(k) * p.pstride + size_t(b) * p.M + m
+                        : p.D + static_cast<size_t>(k - p.splits) * p.dstride + size_t(b) * p.M + m;
+}
+__device__ __forceinline__ int proj_parts(const ProjOut& p) { return p.splits + (p.D ? p.dsplits : 0); }
+
+// All partial loads are issued before the (fixed-order) additions: the reduction
+// costs one memory latency instead of one per partial.
 __device__ __forceinline__ float proj_val(const ProjOut& p, int b, int m) {
     if (p.G) {
         const int r = m / p.g_cols, i = m - r * p.g_cols;
         return p.G[(static_cast<size_t>(r) * p.g_batch + b) * p.g_cols + i];
     }
+    const int n = proj_parts(p);
     float s = 0.0f;
-    for (int k = 0; k < p.splits; ++k) s += p.P[static_cast<size_t>(k) * p.pstride + size_t(b) * p.M + m];
-    if (p.D)
-        for (int k = 0; k < p.dsplits; ++k) s += p.D[static_cast<size_t>(k) * p.dstride + size_t(b) * p.M + m];
+    for (int k0 = 0; k0 < n; k0 += 8) {
+        float t[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) t[j] = (k0 + j < n) ? *proj_ptr(p, k0 + j, b, m) : 0.0f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (k0 + j < n) s += t[j];
+    }
     return s;
 }
 
@@ -101,6 +116,87 @@ __global__ void __launch_bounds__(kNormChunk)
     if (xn_f32) xn_f32[size_t(b) * dim + i] = y;
 }
 
+// ---- default residual + RMSNorm: one launch, chunk partials joined in-kernel ----
+// grid (chunks of kRnChunk, batch) = 128 CTAs at dim 4096 / batch 16, all co-resident.
+// Every CTA adds the projection partials into its chunk of x (float4), writes its
+// double sum of squares, then the CTAs of a request meet on an arrival counter and
+// each re-sums the chunk partials in index order (deterministic, no float atomics).
+constexpr int kRnThreads = 128, kRnChunk = 4 * kRnThreads;
+
+__device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
+    return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+// proj_val for 4 consecutive outputs (same addition order as proj_val -> same bits)
+__device__ __forceinline__ float4 proj_val4(const ProjOut& p, int b, int m) {
+    if (p.G) {
+        const int r = m / p.g_cols, i = m - r * p.g_cols;
+        return *reinterpret_cast<const float4*>(p.G + (static_cast<size_t>(r) * p.g_batch + b) * p.g_cols + i);
+    }
+    const int n = proj_parts(p);
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k0 = 0; k0 < n; k0 += 8) {
+        float4 t[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            t[j] = (k0 + j < n) ? *reinterpret_cast<const float4*>(proj_ptr(p, k0 + j, b, m))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (k0 + j < n) s = f4_add(s, t[j]);
+    }
+    return s;
+}
+
+__global__ void __launch_bounds__(kRnThreads)
+    resid_norm_kernel(float* __restrict__ x, int dim, ProjOut proj, const float* const* __restrict__ norm_w,
+                      uint16_t* __restrict__ xn, int ldxn, float* __restrict__ xn_f32,
+                      unsigned* __restrict__ arrive, double* __restrict__ msq_part) {
+    __shared__ double red_d[32];
+    __shared__ double inv_s;
+    const int b = blockIdx.y, nc = gridDim.x;
+    const int i = blockIdx.x * kRnChunk + 4 * threadIdx.x;
+    const bool on = i < dim;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    float* xb = x + size_t(b) * dim;
+    if (on) {
+        v = *reinterpret_cast<const float4*>(xb + i);
+        if (proj.P || proj.G) {
+            v = f4_add(v, proj_val4(proj, b, proj.col0 + i));
+            *reinterpret_cast<float4*>(xb + i) = v;
+        }
+    }
+    if (!norm_w) return;
+    double sq = static_cast<double>(v.x) * v.x + static_cast<double>(v.y) * v.y +
+                static_cast<double>(v.z) * v.z + static_cast<double>(v.w) * v.w;
+    sq = block_sum(sq, red_d);
+    if (threadIdx.x == 0) {
+        msq_part[size_t(b) * nc + blockIdx.x] = sq;
+        __threadfence();
+        const unsigned old = atomicAdd(arrive + b, 1u);
+        const unsigned target = old - old % unsigned(nc) + unsigned(nc);
+        while (static_cast<int>(*reinterpret_cast<volatile unsigned*>(arrive + b) - target) < 0) __nanosleep(20);
+        __threadfence();
+        double msq = 0.0;
+        for (int k = 0; k < nc; ++k) msq += __ldcg(msq_part + size_t(b) * nc + k);
+        inv_s = 1.0 / sqrt(msq / static_cast<double>(dim) + 1e-12);
+    }
+    __syncthreads();
+    if (!on) return;
+    const double inv = inv_s;
+    const float4 w = *reinterpret_cast<const float4*>(norm_w[b] + i);
+    const float y0 = static_cast<float>(static_cast<double>(v.x) * inv) * w.x;
+    const float y1 = static_cast<float>(static_cast<double>(v.y) * inv) * w.y;
+    const float y2 = static_cast<float>(static_cast<double>(v.z) * inv) * w.z;
+    const float y3 = static_cast<float>(static_cast<double>(v.w) * inv) * w.w;
+    if (xn) {
+        uint2 pk;
+        pk.x = uint32_t(f32_to_bf16(y0)) | (uint32_t(f32_to_bf16(y1)) << 16);
+        pk.y = uint32_t(f32_to_bf16(y2)) | (uint32_t(f32_to_bf16(y3)) << 16);
+        *reinterpret_cast<uint2*>(xn + size_t(b) * ldxn + i) = pk;
+    }
+    if (xn_f32) *reinterpret_cast<float4*>(xn_f32 + size_t(b) * dim + i) = make_float4(y0, y1, y2, y3);
+}
+
 // single-kernel variant: one 1024-thread block per request does the residual add,
 // the double sum of squares (fixed tree) and the normalisation
 constexpr int kFusedNormThreads = 1024;
@@ -159,6 +255,12 @@ __global__ void attn_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos
     const int kh = h / group;
     const int pos = pos_dev[b];
     const float2* rope = a.rope + static_cast<size_t>(pos) * half;
+    const int n_ctx = pos + 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const bool vec = (hd % 4) == 0 && (a.kv_dim % 4) == 0;
+    const bool fast = vec && hd == 128;
+    uint16_t* kc = a.kcache[b] + (static_cast<size_t>(a.layer) * a.max_seq) * a.kv_dim + kh * hd;
+    uint16_t* vc = a.vcache[b] + (static_cast<size_t>(a.layer) * a.max_seq) * a.kv_dim + kh * hd;
 
     // q, k, v of this step (split-K reduction + tenant delta): one element per
     // thread over all 3*hd values, then RoPE on the q and k pairs in smem
@@ -184,8 +286,6 @@ __global__ void attn_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos
         }
     }
     __syncthreads();
-    uint16_t* kc = a.kcache[b] + (static_cast<size_t>(a.layer) * a.max_seq) * a.kv_dim + kh * hd;
-    uint16_t* vc = a.vcache[b] + (static_cast<size_t>(a.layer) * a.max_seq) * a.kv_dim + kh * hd;
     if (h % group == 0) {  // KV append (serve.cpp:261-264), post-RoPE
         for (int i = threadIdx.x; i < hd; i += blockDim.x) {
             kc[static_cast<size_t>(pos) * a.kv_dim + i] = f32_to_bf16(ks[i]);
@@ -194,11 +294,8 @@ __global__ void attn_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos
     }
     // scores (serve.cpp:267-275): one warp per key, lane l owns dims [4l, 4l+4) (+128k),
     // 8-byte loads -> each key row is one coalesced 256-byte warp access
-    const int n_ctx = pos + 1;
     const float inv_sqrt_hd = 1.0f / sqrtf(static_cast<float>(hd));
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const bool vec = (hd % 4) == 0 && (a.kv_dim % 4) == 0;
-    if (vec && hd == 128) {
+    if (fast) {
         // fast path: 8 keys per warp in flight (all loads issued before the math)
         const float q0 = qs[4 * lane], q1 = qs[4 * lane + 1], q2 = qs[4 * lane + 2], q3 = qs[4 * lane + 3];
         for (int j0 = warp; j0 < n_ctx; j0 += nw * 8) {
@@ -261,7 +358,7 @@ __global__ void attn_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos
     // positions j = w (mod nw) for dims [4l, 4l+4), then the warps' partials are
     // added in warp order (fixed) through shared memory
     float* part = scores + a.max_seq;  // [nw][hd]
-    if (vec && hd == 128) {
+    if (fast) {
         // fast path: 8 value rows per warp in flight
         float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
         for (int j0 = warp; j0 < n_ctx; j0 += nw * 8) {
@@ -329,6 +426,145 @@ __global__ void attn_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos
     }
 }
 
+// head_dim 128 path: thread t owns dims [8 (t%16), +8) of rows t/16 + 16 p of a
+// 16*kA2Rows-row chunk, so a CTA has the whole chunk of K and V (64 KB) in flight
+// at once; the first chunk is requested before the q/k/v reduction (the cached
+// rows do not depend on this step). Same math as attn_kernel, different f32
+// summation order.
+constexpr int kA2Threads = 256, kA2Rows = 8, kA2Chunk = 16 * kA2Rows;
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4 u, float (&f)[8]) {
+    f[0] = __uint_as_float(u.x << 16); f[1] = __uint_as_float(u.x & 0xFFFF0000u);
+    f[2] = __uint_as_float(u.y << 16); f[3] = __uint_as_float(u.y & 0xFFFF0000u);
+    f[4] = __uint_as_float(u.z << 16); f[5] = __uint_as_float(u.z & 0xFFFF0000u);
+    f[6] = __uint_as_float(u.w << 16); f[7] = __uint_as_float(u.w & 0xFFFF0000u);
+}
+
+__global__ void __launch_bounds__(kA2Threads, 2)
+    attn128_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos_dev, uint16_t* __restrict__ ctx_out,
+                   int ld_ctx) {
+    constexpr int hd = 128, half = 64;
+    extern __shared__ float sm[];
+    float* qs = sm;                  // hd
+    float* ks = qs + hd;             // hd (this step's key, bf16-rounded)
+    float* vs = ks + hd;             // hd
+    float* part = vs + hd;           // [16][hd]
+    float* scores = part + 16 * hd;  // max_seq
+    __shared__ float red[32];
+    const int h = blockIdx.x, b = blockIdx.y;
+    const int group = a.n_heads / a.n_kv_heads;
+    const int kh = h / group;
+    const int pos = pos_dev[b];
+    const int n_ctx = pos + 1;
+    const int rs = threadIdx.x >> 4, dg = threadIdx.x & 15;
+    uint16_t* kc = a.kcache[b] + (static_cast<size_t>(a.layer) * a.max_seq) * a.kv_dim + kh * hd;
+    uint16_t* vc = a.vcache[b] + (static_cast<size_t>(a.layer) * a.max_seq) * a.kv_dim + kh * hd;
+    auto load_rows = [&](const uint16_t* base, int c0, uint4 (&r)[kA2Rows]) {
+#pragma unroll
+        for (int p = 0; p < kA2Rows; ++p) {
+            const int j = c0 + rs + 16 * p;
+            r[p] = (j < n_ctx && j != pos)
+                       ? *reinterpret_cast<const uint4*>(base + static_cast<size_t>(j) * a.kv_dim + 8 * dg)
+                       : make_uint4(0u, 0u, 0u, 0u);
+        }
+    };
+    uint4 kr[kA2Rows], vr[kA2Rows];
+    load_rows(kc, 0, kr);
+    load_rows(vc, 0, vr);
+
+    // q, k, v of this step (split-K + tenant delta), RoPE (same as attn_kernel)
+    const float2* rope = a.rope + static_cast<size_t>(pos) * half;
+    for (int i = threadIdx.x; i < 3 * hd; i += kA2Threads) {
+        const int which = i / hd, d = i - which * hd;
+        const int col = which == 0 ? h * hd + d : (which == 1 ? a.dim + kh * hd + d : a.dim + a.kv_dim + kh * hd + d);
+        const float v = proj_val(qkv, b, col);
+        (which == 0 ? qs : (which == 1 ? ks : vs))[d] = which == 2 ? bf16_to_f32(f32_to_bf16(v)) : v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * half) {
+        const int i = threadIdx.x, pi = i % half;
+        float* buf = i < half ? qs : ks;
+        const float2 cs = rope[pi];
+        const float v0 = buf[2 * pi], v1 = buf[2 * pi + 1];
+        const float r0 = v0 * cs.x - v1 * cs.y, r1 = v0 * cs.y + v1 * cs.x;
+        if (i < half) {
+            buf[2 * pi] = r0;
+            buf[2 * pi + 1] = r1;
+        } else {
+            buf[2 * pi] = bf16_to_f32(f32_to_bf16(r0));
+            buf[2 * pi + 1] = bf16_to_f32(f32_to_bf16(r1));
+        }
+    }
+    __syncthreads();
+    if (h % group == 0 && threadIdx.x < hd) {  // KV append (serve.cpp:261-264), post-RoPE
+        kc[static_cast<size_t>(pos) * a.kv_dim + threadIdx.x] = f32_to_bf16(ks[threadIdx.x]);
+        vc[static_cast<size_t>(pos) * a.kv_dim + threadIdx.x] = f32_to_bf16(vs[threadIdx.x]);
+    }
+    // scores (serve.cpp:267-275)
+    const float inv_sqrt_hd = 1.0f / sqrtf(static_cast<float>(hd));
+    float q[8], kn[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        q[e] = qs[8 * dg + e];
+        kn[e] = ks[8 * dg + e];
+    }
+    for (int c0 = 0; c0 < n_ctx; c0 += kA2Chunk) {
+        if (c0) load_rows(kc, c0, kr);
+#pragma unroll
+        for (int p = 0; p < kA2Rows; ++p) {
+            const int j = c0 + rs + 16 * p;
+            float k8[8];
+            bf16x8_to_f32(kr[p], k8);
+            float acc = 0.0f;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc += q[e] * (j == pos ? kn[e] : k8[e]);
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (dg == 0 && j < n_ctx) scores[j] = acc * inv_sqrt_hd;
+        }
+    }
+    __syncthreads();
+    // softmax (nn_ops.hpp:48-57)
+    float mx = -INFINITY;
+    for (int j = threadIdx.x; j < n_ctx; j += kA2Threads) mx = fmaxf(mx, scores[j]);
+    mx = block_max(mx, red);
+    float sum = 0.0f;
+    for (int j = threadIdx.x; j < n_ctx; j += kA2Threads) {
+        const float e = expf(scores[j] - mx);
+        scores[j] = e;
+        sum += e;
+    }
+    sum = block_sum(sum, red);
+    __syncthreads();
+    // ctx (serve.cpp:276-281): p_j = e_j / sum; row-slot partials added in slot order
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float vn[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) vn[e] = vs[8 * dg + e];
+    for (int c0 = 0; c0 < n_ctx; c0 += kA2Chunk) {
+        if (c0) load_rows(vc, c0, vr);
+#pragma unroll
+        for (int p = 0; p < kA2Rows; ++p) {
+            const int j = c0 + rs + 16 * p;
+            if (j >= n_ctx) break;
+            const float pj = scores[j] / sum;
+            float v8[8];
+            bf16x8_to_f32(vr[p], v8);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] += pj * (j == pos ? vn[e] : v8[e]);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) part[rs * hd + 8 * dg + e] = acc[e];
+    __syncthreads();
+    if (threadIdx.x < hd) {
+        float t = 0.0f;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) t += part[r * hd + threadIdx.x];
+        ctx_out[size_t(b) * ld_ctx + h * hd + threadIdx.x] = f32_to_bf16(t);
+    }
+}
+
 // act = silu(gate) * up (serve.cpp:301-302)
 __global__ void silu_kernel(ProjOut gu, int inter, uint16_t* __restrict__ act, int ld_act) {
     const int b = blockIdx.y;
@@ -337,6 +573,19 @@ __global__ void silu_kernel(ProjOut gu, int inter, uint16_t* __restrict__ act, i
         const float u = proj_val(gu, b, inter + i);
         const float s = g / (1.0f + expf(-g));
         act[size_t(b) * ld_act + i] = f32_to_bf16(s * u);
+    }
+}
+// 4 outputs per thread (aligned shapes), same per-element arithmetic
+__global__ void silu4_kernel(ProjOut gu, int inter, uint16_t* __restrict__ act, int ld_act) {
+    const int b = blockIdx.y;
+    for (int i = 4 * (blockIdx.x * blockDim.x + threadIdx.x); i < inter; i += 4 * gridDim.x * blockDim.x) {
+        const float4 g = proj_val4(gu, b, i);
+        const float4 u = proj_val4(gu, b, inter + i);
+        auto f = [](float gv, float uv) { return f32_to_bf16(gv / (1.0f + expf(-gv)) * uv); };
+        uint2 pk;
+        pk.x = uint32_t(f(g.x, u.x)) | (uint32_t(f(g.y, u.y)) << 16);
+        pk.y = uint32_t(f(g.z, u.z)) | (uint32_t(f(g.w, u.w)) << 16);
+        *reinterpret_cast<uint2*>(act + size_t(b) * ld_act + i) = pk;
     }
 }
 
@@ -408,8 +657,37 @@ void gather_transpose_launch(const uint16_t* src, int world, int batch, int n_l,
 
 int norm_chunks(int dim) { return (dim + kNormChunk - 1) / kNormChunk; }
 
+namespace {
+bool proj_vec4_ok(const ProjOut& p) {
+    if (p.G) return p.g_cols % 4 == 0 && reinterpret_cast<uintptr_t>(p.G) % 16 == 0;
+    if (!p.P) return true;
+    return p.M % 4 == 0 && p.col0 % 4 == 0 && p.pstride % 4 == 0 && reinterpret_cast<uintptr_t>(p.P) % 16 == 0 &&
+           (!p.D || (p.dstride % 4 == 0 && reinterpret_cast<uintptr_t>(p.D) % 16 == 0));
+}
+}  // namespace
+
+size_t norm_ws_bytes(int batch, int dim) {
+    const size_t cnt = (size_t(batch) * sizeof(unsigned) + 255) / 256 * 256;
+    return cnt + size_t(batch) * std::max(norm_chunks(dim), (dim + kRnChunk - 1) / kRnChunk) * sizeof(double);
+}
+
 void resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const float* const* norm_w,
-                       uint16_t* xn, int ldxn, float* xn_f32, double* msq_ws, cudaStream_t s) {
+                       uint16_t* xn, int ldxn, float* xn_f32, void* ws, cudaStream_t s) {
+    unsigned* arrive = static_cast<unsigned*>(ws);
+    double* msq_ws = reinterpret_cast<double*>(static_cast<char*>(ws) +
+                                               (size_t(batch) * sizeof(unsigned) + 255) / 256 * 256);
+    // one-launch path: the CTAs of a request meet on an arrival counter, so the whole
+    // grid must be co-resident (<= 8 CTAs per SM here) -> bounded grid size
+    const int nc = (dim + kRnChunk - 1) / kRnChunk;
+    static const bool two_phase = std::getenv("BD_NORM_TWO") && std::getenv("BD_NORM_TWO")[0] == '1';
+    if (!two_phase && dim % 4 == 0 && ldxn % 4 == 0 && proj_vec4_ok(proj) &&
+        size_t(nc) * batch <= size_t(kNumSMs) * 8) {
+        resid_norm_kernel<<<dim3(nc, batch), kRnThreads, 0, s>>>(x, dim, proj, norm_w, xn, ldxn, xn_f32,
+                                                                   arrive, msq_ws);
+        note_launch();
+        BD_CUDA(cudaGetLastError());
+        return;
+    }
     // One-launch variant (16 CTAs) measured slower than the two-phase, 16x wider
     // grid at batch 16 (1.22 vs 0.73 ms/step); kept for BD_NORM_ONE=1 experiments.
     static const bool one = std::getenv("BD_NORM_ONE") && std::getenv("BD_NORM_ONE")[0] == '1';
@@ -431,6 +709,19 @@ void resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const 
 
 void attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int batch,
                  uint16_t* ctx, int ld_ctx, cudaStream_t s) {
+    static const bool old = std::getenv("BD_ATTN_OLD") && std::getenv("BD_ATTN_OLD")[0] == '1';
+    if (!old && a.hd == 128 && a.kv_dim % 8 == 0 && a.dim % 8 == 0) {
+        const size_t smem = (3 * 128 + 16 * 128 + a.max_seq) * sizeof(float);
+        static bool attr2 = false;
+        if (!attr2) {
+            BD_CUDA(cudaFuncSetAttribute(attn128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            attr2 = true;
+        }
+        attn128_kernel<<<dim3(a.n_heads, batch), kA2Threads, smem, s>>>(qkv, a, pos_dev, ctx, ld_ctx);
+        note_launch();
+        BD_CUDA(cudaGetLastError());
+        return;
+    }
     constexpr int kAttnThreads = 256;
     const size_t smem = (3 * a.hd + a.max_seq + (kAttnThreads / 32) * a.hd) * sizeof(float);
     static bool attr = false;
@@ -444,8 +735,13 @@ void attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int 
 }
 
 void silu_launch(const ProjOut& gu, int batch, int inter, uint16_t* act, int ld_act, cudaStream_t s) {
-    const int bx = std::max(1, std::min((inter + 255) / 256, 64));
-    silu_kernel<<<dim3(bx, batch), 256, 0, s>>>(gu, inter, act, ld_act);
+    if (inter % 4 == 0 && ld_act % 4 == 0 && proj_vec4_ok(gu)) {
+        const int bx = std::max(1, std::min((inter / 4 + 127) / 128, 64));
+        silu4_kernel<<<dim3(bx, batch), 128, 0, s>>>(gu, inter, act, ld_act);
+    } else {
+        const int bx = std::max(1, std::min((inter + 255) / 256, 64));
+        silu_kernel<<<dim3(bx, batch), 256, 0, s>>>(gu, inter, act, ld_act);
+    }
     note_launch();
     BD_CUDA(cudaGetLastError());
 }

@@ -35,10 +35,12 @@ struct AttnArgs {
     const float2* rope;       // [max_seq][hd/2] (cos, sin)
 };
 
-// msq_ws: batch * norm_chunks(dim) doubles of scratch
+// ws: norm_ws_bytes(batch, dim) bytes, zeroed once at allocation (arrival counters
+// + chunk sums of squares); launches using one ws must be stream-ordered
 int norm_chunks(int dim);
+size_t norm_ws_bytes(int batch, int dim);
 void resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const float* const* norm_w,
-                       uint16_t* xn, int ldxn, float* xn_f32, double* msq_ws, cudaStream_t s);
+                       uint16_t* xn, int ldxn, float* xn_f32, void* ws, cudaStream_t s);
 void attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int batch,
                  uint16_t* ctx, int ld_ctx, cudaStream_t s);
 void silu_launch(const ProjOut& gu, int batch, int inter, uint16_t* act, int ld_act, cudaStream_t s);

@@ -171,7 +171,7 @@ struct PoolImpl {
     // workspaces (sized for ws_B)
     int ws_B = 0;
     float *x = nullptr, *xn_f32 = nullptr, *P = nullptr, *D = nullptr, *logits = nullptr;
-    double* msq = nullptr;  // per-request chunk sums of squares (RMSNorm)
+    void* msq = nullptr;  // RMSNorm workspace (norm_ws_bytes: arrival counters + chunk sums)
     // tensor parallel (world > 1)
     ncclComm_t comm = nullptr;
     uint16_t *ctx_loc = nullptr, *act_loc = nullptr, *gath16 = nullptr;
@@ -187,6 +187,9 @@ struct PoolImpl {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool concurrent_k23 = true;      // BD_SERIAL=1 disables
     bool use_graphs = true;
+    // timing experiments only (results are wrong): BD_SKIP bitmask drops launches of
+    // 1 norm, 2 attention, 4 silu, 8 K3 delta, 16 K2 gemm
+    int skip = 0;
     bool use_fused = true;
     std::string delta_mode = "auto";  // auto | lut | fused | units (BD_DELTA)
 
@@ -258,6 +261,7 @@ struct PoolImpl {
         BD_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         BD_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
         if (const char* e = std::getenv("BD_NO_GRAPH")) use_graphs = (e[0] == '0');
+        if (const char* e = std::getenv("BD_SKIP")) skip = std::atoi(e);
         if (const char* e = std::getenv("BD_NO_FUSED")) use_fused = (e[0] == '0');
         if (!use_fused) delta_mode = "units";
         if (const char* e = std::getenv("BD_DELTA")) delta_mode = e;
@@ -679,7 +683,8 @@ struct PoolImpl {
         P_elems = 33ull * ws_B * Mmax;
         P = dmalloc<float>(P_elems, &ws_allocs);
         logits = dmalloc<float>(ws_B * a.vocab, &ws_allocs);
-        msq = dmalloc<double>(size_t(ws_B) * norm_chunks(int(a.dim)), &ws_allocs);
+        msq = dmalloc<char>(norm_ws_bytes(int(ws_B), int(a.dim)), &ws_allocs);
+        BD_CUDA(cudaMemset(msq, 0, norm_ws_bytes(int(ws_B), int(a.dim))));
         if (world > 1) {
             ctx_loc = dmalloc<uint16_t>(size_t(ws_B) * q_l, &ws_allocs);
             act_loc = dmalloc<uint16_t>(size_t(ws_B) * inter_l, &ws_allocs);
@@ -1047,8 +1052,8 @@ struct PoolImpl {
                 prof(BD_PROF_FUSED_QKV + group, s, [&] {
                     BD_CUDA(cudaEventRecord(ev_fork, s));
                     BD_CUDA(cudaStreamWaitEvent(stream2, ev_fork, 0));
-                    lut_launch(p.lut[l][group].prm, X, D, s);
-                    base_gemm_launch(g, mw, mx, P, stream2);
+                    if (!(skip & 8)) lut_launch(p.lut[l][group].prm, X, D, s);
+                    if (!(skip & 16)) base_gemm_launch(g, mw, mx, P, stream2);
                     BD_CUDA(cudaEventRecord(ev_join, stream2));
                     BD_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
                 });
@@ -1103,13 +1108,13 @@ struct PoolImpl {
         for (uint64_t l = 0; l < nL; ++l) {
             const LayerW& W = L[l];
             // x += down(prev); xn = norm1(x)   (x and xn replicated on every rank)
-            prof(BD_PROF_NORM, s, [&] {
+            if (!(skip & 1)) prof(BD_PROF_NORM, s, [&] {
                 resid_norm_launch(x, B, int(a.dim), prev, p.d_norm + (2 * l) * B, xn, int(ld_dim),
                                   nullptr, msq, s);
             });
             linear(p, l, 0, p.g_qkv, W.m_qkv, p.x_xn, p.units[l][0], xn, int(ld_dim), int(a.dim), B, s);
             aa.layer = int(l);
-            prof(BD_PROF_ATTN, s, [&] {
+            if (!(skip & 2)) prof(BD_PROF_ATTN, s, [&] {
                 attn_launch(group_out(p, l, 0, p.g_qkv), aa, p.d_pos, B, tp ? ctx_loc : ctx,
                             tp ? int(q_l) : int(ld_dim), s);
             });
@@ -1117,12 +1122,12 @@ struct PoolImpl {
             linear(p, l, 1, p.g_o, W.m_o, p.x_ctx, p.units[l][1], ctx, int(ld_dim), int(a.dim), B, s);
             const ProjOut o_out = tp ? exchange_f32(group_out(p, l, 1, p.g_o), B, int(dim_l), s)
                                      : group_out(p, l, 1, p.g_o);
-            prof(BD_PROF_NORM, s, [&] {
+            if (!(skip & 1)) prof(BD_PROF_NORM, s, [&] {
                 resid_norm_launch(x, B, int(a.dim), o_out, p.d_norm + (2 * l + 1) * B, xn, int(ld_dim),
                                   nullptr, msq, s);
             });
             linear(p, l, 2, p.g_gu, W.m_gu, p.x_xn, p.units[l][2], xn, int(ld_dim), int(a.dim), B, s);
-            prof(BD_PROF_SILU, s, [&] {
+            if (!(skip & 4)) prof(BD_PROF_SILU, s, [&] {
                 silu_launch(group_out(p, l, 2, p.g_gu), B, int(inter_l), tp ? act_loc : act,
                             tp ? int(inter_l) : int(ld_inter), s);
             });
