@@ -426,12 +426,13 @@ __global__ void attn_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos
     }
 }
 
-// head_dim 128 path: thread t owns dims [8 (t%16), +8) of rows t/16 + 16 p of a
-// 16*kA2Rows-row chunk, so a CTA has the whole chunk of K and V (64 KB) in flight
-// at once; the first chunk is requested before the q/k/v reduction (the cached
-// rows do not depend on this step). Same math as attn_kernel, different f32
-// summation order.
-constexpr int kA2Threads = 256, kA2Rows = 8, kA2Chunk = 16 * kA2Rows;
+// head_dim 128 path. The cached K and V rows of the (request, head) are copied
+// into shared memory with cp.async at kernel start (they do not depend on this
+// step), so the whole context is in flight at once while q/k/v are reduced; a
+// context longer than the staging buffer is processed in chunks (K pass, then
+// V pass). Thread t owns dims [8 (t%16), +8) of rows t/16 (mod 16). Same math
+// as attn_kernel, different f32 summation order.
+constexpr int kA2Threads = 256;
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4 u, float (&f)[8]) {
     f[0] = __uint_as_float(u.x << 16); f[1] = __uint_as_float(u.x & 0xFFFF0000u);
@@ -439,17 +440,30 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4 u, float (&f)[8]) {
     f[4] = __uint_as_float(u.z << 16); f[5] = __uint_as_float(u.z & 0xFFFF0000u);
     f[6] = __uint_as_float(u.w << 16); f[7] = __uint_as_float(u.w & 0xFFFF0000u);
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-__global__ void __launch_bounds__(kA2Threads, 2)
+// rows [r0, r0 + n) of one head (256 B each, row stride ld elements) -> dst[n][128]
+__device__ __forceinline__ void stage_rows(uint16_t* dst, const uint16_t* src, int r0, int n, int ld) {
+    for (int i = threadIdx.x; i < n * 16; i += kA2Threads) {
+        const int r = i >> 4, c = i & 15;
+        cp_async16(dst + r * 128 + 8 * c, src + static_cast<size_t>(r0 + r) * ld + 8 * c);
+    }
+}
+
+__global__ void __launch_bounds__(kA2Threads)
     attn128_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos_dev, uint16_t* __restrict__ ctx_out,
-                   int ld_ctx) {
+                   int ld_ctx, int stage_rows_max) {
     constexpr int hd = 128, half = 64;
-    extern __shared__ float sm[];
+    extern __shared__ __align__(16) float sm[];
     float* qs = sm;                  // hd
     float* ks = qs + hd;             // hd (this step's key, bf16-rounded)
     float* vs = ks + hd;             // hd
-    float* part = vs + hd;           // [16][hd]
-    float* scores = part + 16 * hd;  // max_seq
+    uint16_t* st = reinterpret_cast<uint16_t*>(vs + hd);            // [stage_rows_max][hd]: K, then V, then partials
+    float* scores = reinterpret_cast<float*>(st + stage_rows_max * hd);  // max_seq
     __shared__ float red[32];
     const int h = blockIdx.x, b = blockIdx.y;
     const int group = a.n_heads / a.n_kv_heads;
@@ -459,18 +473,8 @@ __global__ void __launch_bounds__(kA2Threads, 2)
     const int rs = threadIdx.x >> 4, dg = threadIdx.x & 15;
     uint16_t* kc = a.kcache[b] + (static_cast<size_t>(a.layer) * a.max_seq) * a.kv_dim + kh * hd;
     uint16_t* vc = a.vcache[b] + (static_cast<size_t>(a.layer) * a.max_seq) * a.kv_dim + kh * hd;
-    auto load_rows = [&](const uint16_t* base, int c0, uint4 (&r)[kA2Rows]) {
-#pragma unroll
-        for (int p = 0; p < kA2Rows; ++p) {
-            const int j = c0 + rs + 16 * p;
-            r[p] = (j < n_ctx && j != pos)
-                       ? *reinterpret_cast<const uint4*>(base + static_cast<size_t>(j) * a.kv_dim + 8 * dg)
-                       : make_uint4(0u, 0u, 0u, 0u);
-        }
-    };
-    uint4 kr[kA2Rows], vr[kA2Rows];
-    load_rows(kc, 0, kr);
-    load_rows(vc, 0, vr);
+    // row `pos` is this step's own key/value (taken from smem below, never read from the cache)
+    stage_rows(st, kc, 0, min(n_ctx, stage_rows_max), a.kv_dim);
 
     // q, k, v of this step (split-K + tenant delta), RoPE (same as attn_kernel)
     const float2* rope = a.rope + static_cast<size_t>(pos) * half;
@@ -495,6 +499,7 @@ __global__ void __launch_bounds__(kA2Threads, 2)
             buf[2 * pi + 1] = bf16_to_f32(f32_to_bf16(r1));
         }
     }
+    cp_async_wait_all();
     __syncthreads();
     if (h % group == 0 && threadIdx.x < hd) {  // KV append (serve.cpp:261-264), post-RoPE
         kc[static_cast<size_t>(pos) * a.kv_dim + threadIdx.x] = f32_to_bf16(ks[threadIdx.x]);
@@ -508,22 +513,30 @@ __global__ void __launch_bounds__(kA2Threads, 2)
         q[e] = qs[8 * dg + e];
         kn[e] = ks[8 * dg + e];
     }
-    for (int c0 = 0; c0 < n_ctx; c0 += kA2Chunk) {
-        if (c0) load_rows(kc, c0, kr);
-#pragma unroll
-        for (int p = 0; p < kA2Rows; ++p) {
-            const int j = c0 + rs + 16 * p;
+    for (int c0 = 0; c0 < n_ctx; c0 += stage_rows_max) {
+        const int nr = min(stage_rows_max, n_ctx - c0);
+        if (c0) {
+            __syncthreads();  // previous chunk consumed
+            stage_rows(st, kc, c0, nr, a.kv_dim);
+            cp_async_wait_all();
+            __syncthreads();
+        }
+        for (int rb = 0; rb < nr; rb += 16) {  // warp-uniform trip count (shuffles below)
+            const int r = rb + rs, j = c0 + r;
             float k8[8];
-            bf16x8_to_f32(kr[p], k8);
+            bf16x8_to_f32(r < nr ? *reinterpret_cast<const uint4*>(st + r * hd + 8 * dg) : make_uint4(0u, 0u, 0u, 0u),
+                          k8);
             float acc = 0.0f;
 #pragma unroll
             for (int e = 0; e < 8; ++e) acc += q[e] * (j == pos ? kn[e] : k8[e]);
 #pragma unroll
             for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (dg == 0 && j < n_ctx) scores[j] = acc * inv_sqrt_hd;
+            if (dg == 0 && r < nr) scores[j] = acc * inv_sqrt_hd;
         }
     }
     __syncthreads();
+    // the first V chunk streams in while the softmax runs
+    stage_rows(st, vc, 0, min(n_ctx, stage_rows_max), a.kv_dim);
     // softmax (nn_ops.hpp:48-57)
     float mx = -INFINITY;
     for (int j = threadIdx.x; j < n_ctx; j += kA2Threads) mx = fmaxf(mx, scores[j]);
@@ -535,25 +548,32 @@ __global__ void __launch_bounds__(kA2Threads, 2)
         sum += e;
     }
     sum = block_sum(sum, red);
+    cp_async_wait_all();
     __syncthreads();
     // ctx (serve.cpp:276-281): p_j = e_j / sum; row-slot partials added in slot order
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     float vn[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) vn[e] = vs[8 * dg + e];
-    for (int c0 = 0; c0 < n_ctx; c0 += kA2Chunk) {
-        if (c0) load_rows(vc, c0, vr);
-#pragma unroll
-        for (int p = 0; p < kA2Rows; ++p) {
-            const int j = c0 + rs + 16 * p;
-            if (j >= n_ctx) break;
+    for (int c0 = 0; c0 < n_ctx; c0 += stage_rows_max) {
+        const int nr = min(stage_rows_max, n_ctx - c0);
+        if (c0) {
+            __syncthreads();
+            stage_rows(st, vc, c0, nr, a.kv_dim);
+            cp_async_wait_all();
+            __syncthreads();
+        }
+        for (int r = rs; r < nr; r += 16) {
+            const int j = c0 + r;
             const float pj = scores[j] / sum;
             float v8[8];
-            bf16x8_to_f32(vr[p], v8);
+            bf16x8_to_f32(*reinterpret_cast<const uint4*>(st + r * hd + 8 * dg), v8);
 #pragma unroll
             for (int e = 0; e < 8; ++e) acc[e] += pj * (j == pos ? vn[e] : v8[e]);
         }
     }
+    __syncthreads();  // staging buffer reused for the row-slot partials [16][hd] f32
+    float* part = reinterpret_cast<float*>(st);
 #pragma unroll
     for (int e = 0; e < 8; ++e) part[rs * hd + 8 * dg + e] = acc[e];
     __syncthreads();
@@ -711,13 +731,17 @@ void attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int 
                  uint16_t* ctx, int ld_ctx, cudaStream_t s) {
     static const bool old = std::getenv("BD_ATTN_OLD") && std::getenv("BD_ATTN_OLD")[0] == '1';
     if (!old && a.hd == 128 && a.kv_dim % 8 == 0 && a.dim % 8 == 0) {
-        const size_t smem = (3 * 128 + 16 * 128 + a.max_seq) * sizeof(float);
+        // one staging buffer of up to 192 rows (48 KB: K, then V): four CTAs per SM,
+        // so batch x heads = 512 CTAs run as a single wave on 148 SMs
+        const int rows = std::min(192, std::max(32, a.max_seq));
+        const size_t smem = (3 * 128 + size_t(a.max_seq)) * sizeof(float) + size_t(rows) * 128 * 2;
         static bool attr2 = false;
         if (!attr2) {
-            BD_CUDA(cudaFuncSetAttribute(attn128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            BD_CUDA(cudaFuncSetAttribute(attn128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
             attr2 = true;
         }
-        attn128_kernel<<<dim3(a.n_heads, batch), kA2Threads, smem, s>>>(qkv, a, pos_dev, ctx, ld_ctx);
+        require(smem <= 220 * 1024, BD_ERR_BAD_ARGUMENT, "attention: max_seq too large for the score buffer");
+        attn128_kernel<<<dim3(a.n_heads, batch), kA2Threads, smem, s>>>(qkv, a, pos_dev, ctx, ld_ctx, rows);
         note_launch();
         BD_CUDA(cudaGetLastError());
         return;

@@ -243,9 +243,10 @@ def _random_entries(arch, rng, alpha=2e-3, raw_sigma=1e-2):
 
 
 def test_head_dim_128_long_context_matches_port(cuda, port):
-    """The head_dim-128 attention kernel (the Llama-2-7B shape) over > 128 cached
-    positions (two K/V chunks), two tenants, against the port on a bf16 backbone."""
-    arch = dict(vocab=64, dim=256, n_layers=1, n_heads=2, intermediate=512, max_seq=160,
+    """The head_dim-128 attention kernel (the Llama-2-7B shape) past its 192-row
+    shared-memory staging (two K/V chunks), two tenants, against the port on a
+    bf16 backbone."""
+    arch = dict(vocab=64, dim=256, n_layers=1, n_heads=2, intermediate=512, max_seq=220,
                 rope_theta=10000.0, kv_dim=256)
     rng = np.random.default_rng(7)
     tens = {}
@@ -266,11 +267,11 @@ def test_head_dim_128_long_context_matches_port(cuda, port):
     flat = np.concatenate([tens[n].reshape(-1) for n in names])
     kc = [np.zeros((1, arch["max_seq"], arch["kv_dim"]), np.float32) for _ in range(2)]
     vc = [np.zeros_like(k) for k in kc]
-    toks = rng.integers(0, arch["vocab"], 140)
+    toks = rng.integers(0, arch["vocab"], 200)
     for pos, tok in enumerate(toks):
         got = pool.decode_step([(r, int(tok), pos) for r in rids])
         want = port.decode(arch, flat, port_ents, [0, 1], [int(tok)] * 2, [pos] * 2, kc, vc)
-        if pos % 16 == 0 or pos >= 126:
+        if pos % 16 == 0 or pos >= 188:
             for i in range(2):
                 # bf16 activations/KV against the f32 port: 4e-3..1.3e-2 measured here,
                 # identical with the generic attention kernel (BD_ATTN_OLD=1)

@@ -1,6 +1,6 @@
-python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 300 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
 for sk in 0 29 0; do
-BD_SKIP=$sk python bench.py --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/v.json 2>/dev/null
+BD_SKIP=$sk timeout 200 python bench.py --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/v.json 2>gpurun_out/v.err
 python -c "
-import json;d=json.load(open('gpurun_out/v.json'));print('skip=$sk', d['value'],d['ms_per_step'])"
+import json;d=json.load(open('gpurun_out/v.json'));print('skip=$sk', d['value'],d['ms_per_step'])" 2>/dev/null || tail -3 gpurun_out/v.err
 done
