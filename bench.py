@@ -77,19 +77,28 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi needs a moment to start: wait for its first sample so the
+            # timed region is covered
+            t_end = time.time() + 10.0
+            while not self.samples and time.time() < t_end and self.proc.poll() is None:
+                time.sleep(0.02)
         except FileNotFoundError:
             self.proc = None
         return self
+
+    def mark(self, which):
+        """Bracket the timed region (wall clock); summary() keeps samples inside it."""
+        setattr(self, which, time.time())
 
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 7:
-                self.samples.append(parts)
+                self.samples.append([time.time()] + parts)
 
     def __exit__(self, *a):
         if self.proc:
@@ -97,15 +106,23 @@ class ClockSampler:
             self.proc.wait(timeout=5)
 
     def summary(self):
-        if not self.samples:
+        t0, t1 = getattr(self, "t0", None), getattr(self, "t1", None)
+        inside = [s[1:] for s in self.samples if t0 is not None and t0 <= s[0] <= (t1 or 1e30)]
+        where = "timed_region"
+        if not inside and self.samples:
+            # region shorter than the sampling period: the sample nearest its end (under load)
+            before = [s for s in self.samples if t1 is None or s[0] <= t1 + 0.1]
+            inside = [(before or self.samples)[-1][1:]]
+            where = "nearest_to_region"
+        if not inside:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        sm = [float(s[0]) for s in inside if s[0].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[3 + i]
+        reasons = sorted({names[i] for s in inside for i in range(4) if "Active" in s[3 + i]
                           and "Not" not in s[3 + i]})
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "sm_max_mhz": float(inside[0][1]) if inside[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(inside), "where": where}
 
 
 def algorithmic_bytes(arch, tenants, batch):
@@ -221,11 +238,13 @@ def run_ours(args, rank, world, dev):
     launches0 = bd.launch_count()
     with ClockSampler(dev.index or 0) as clk:
         torch.cuda.synchronize()
+        clk.mark("t0")
         e0.record(stream)
         for _ in range(args.steps):
             step(x, y)
         e1.record(stream)
         torch.cuda.synchronize()
+        clk.mark("t1")
     dist_barrier(world)
     ms = e0.elapsed_time(e1)
     ms_max = dist_max(ms, world, dev)
@@ -411,7 +430,7 @@ def dist_max(v, world, dev):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="l7_stack", choices=sorted(WORKLOADS))
