@@ -1,6 +1,7 @@
 // extern "C" implementation of include/bitdelta/capi.h. No exception crosses
 // the ABI: every entry point maps bd::Failure to its status code and stores the
 // message for bd_last_error(); CUDA errors map to BD_ERR_CUDA.
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
@@ -97,6 +98,62 @@ void multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int32_
     const std::string mode = mode_env ? mode_env : "auto";
     size_t max_per_tenant = 0;
     for (int t : order) max_per_tenant = std::max(max_per_tenant, by_t[t].size());
+    // ---- K23: base GEMM + FP4 tensor-core deltas in one persistent kernel ----
+    bool aligned16 = in_dim % 128 == 0 && out_dim % 128 == 0;
+    for (int t : order) aligned16 &= (reinterpret_cast<uintptr_t>(tenant_bits[t]) % 16) == 0;
+    if ((mode == "mt4" || mode == "auto") && aligned16 && !order.empty() && batch <= 64) {
+        Mt4Params prm{};
+        prm.n_subs = 1;
+        prm.sub_row0[0] = 0;
+        prm.sub_row0[1] = int(out_dim);
+        std::vector<CUtensorMap> maps;
+        bool ok = true;
+        // canonical slot order (tenant id): the schedule, and so every output bit, does not
+        // depend on the order of the requests in the batch (test_serve.cpp:169-190)
+        std::vector<int> sorted_t(order);
+        std::sort(sorted_t.begin(), sorted_t.end());
+        for (int t : sorted_t) {
+            const auto& rq = by_t[t];
+            const int mi = int(maps.size());
+            maps.push_back(tmap_bits4(tenant_bits[t], out_dim, in_dim));
+            for (size_t c = 0; c < rq.size(); c += kMt4MaxReq) {
+                if (prm.n_slots >= kMt4MaxSlots) { ok = false; break; }
+                Mt4Slot& sl = prm.slots[prm.n_slots++];
+                sl.n_req = int(std::min<size_t>(kMt4MaxReq, rq.size() - c));
+                for (int q = 0; q < sl.n_req; ++q) sl.req[q] = rq[c + q];
+                sl.alpha[0] = tenant_alpha[t];
+                sl.map_idx[0] = mi;
+            }
+        }
+        if (ok && plan_mt4(prm, out_dim, in_dim, batch)) {
+            const int kpad = xp_k_pad(int(in_dim));
+            const int ldxp = kpad / 2, ldxs = kpad / 32;
+            const size_t sz_p = sizeof(float) * prm.splits * batch * out_dim;
+            const size_t sz_xp = size_t(8) * batch * ldxp, sz_xs = size_t(8) * batch * ldxs;
+            const size_t sz_m = maps.size() * sizeof(CUtensorMap);
+            char* ws = nullptr;
+            BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), sz_p + sz_xp + sz_xs + sz_m + 1024, stream));
+            char* cur = ws;
+            auto take = [&](size_t n) { char* r = cur; cur += (n + 255) & ~size_t(255); return r; };
+            float* P = reinterpret_cast<float*>(take(sz_p));
+            uint8_t* Xp = reinterpret_cast<uint8_t*>(take(sz_xp));
+            uint8_t* Xs = reinterpret_cast<uint8_t*>(take(sz_xs));
+            CUtensorMap* dmaps = reinterpret_cast<CUtensorMap*>(take(sz_m));
+            BD_CUDA(cudaMemcpyAsync(dmaps, maps.data(), sz_m, cudaMemcpyHostToDevice, stream));
+            BD_CUDA(cudaStreamSynchronize(stream));  // host staging consumed
+            prm.map_w = mw;
+            prm.map_x = tmap_acts(X, batch, in_dim, in_dim, prm.bn);
+            prm.map_xp = tmap_xp(Xp, 8 * batch, ldxp);
+            prm.map_xs = tmap_xs(Xs, 8 * batch, ldxs);
+            prm.bits_maps = dmaps;
+            prm.partial = P;
+            xp_prep_launch(X, int(in_dim), int(in_dim), batch, Xp, ldxp, Xs, ldxs, stream);
+            mt4_launch(prm, stream);
+            combine_launch(P, prm.splits, nullptr, batch, int(out_dim), Y, stream);
+            BD_CUDA(cudaFreeAsync(ws, stream));
+            return;
+        }
+    }
     // ---- byte-LUT path (few requests per tenant): tcgen05 base GEMM + K3 LUT ----
     if ((mode == "lut" || (mode == "auto" && max_per_tenant <= 4)) && !order.empty() &&
         batch <= kLutMaxJobs) {

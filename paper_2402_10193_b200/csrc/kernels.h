@@ -98,6 +98,38 @@ void xq_prep_launch(const void* X, int ldx, int K, int batch, const int* xq_row_
 CUtensorMap tmap_bits(const uint8_t* bits, uint64_t rows, uint64_t cols);
 CUtensorMap tmap_xq(const int8_t* Xq, int rows, uint64_t K, uint64_t ldq);
 
+// ---- K23: base GEMM + tenant deltas as FP4 (kind::mxf4) MMAs in one persistent kernel (mt4.cu) ----
+constexpr int kMt4MaxSlots = 64;
+constexpr int kMt4MaxReq = 4;   // requests per slot (MMA N = 8 pieces x n_req <= 32)
+constexpr int kMt4MaxSubs = 3;
+struct Mt4Slot {
+    int n_req;
+    int req[kMt4MaxReq];          // batch indices (Xp/Xs rows 8*req .. 8*req+7)
+    float alpha[kMt4MaxSubs];     // per stacked sub-matrix
+    int map_idx[kMt4MaxSubs];     // index into the bits tensor-map table
+};
+struct Mt4Params {
+    CUtensorMap map_w, map_x, map_xp, map_xs;
+    const CUtensorMap* bits_maps;  // device table (tmap_bits4)
+    float* partial;                // [splits][batch][M]
+    long long total_stages;
+    int M, K, batch, bn, nr_max, n_subs, n_slots;
+    int sub_row0[kMt4MaxSubs + 1];
+    int kb_base, kc_plane, stages_per_tile, grid, splits, stages, smem;
+    Mt4Slot slots[kMt4MaxSlots];
+};
+// Fills the schedule (stages per tile, persistent grid, splits, smem ring); false if unsupported.
+bool plan_mt4(Mt4Params& p, uint64_t M, uint64_t K, int batch);
+void mt4_launch(const Mt4Params& p, cudaStream_t stream);
+// K padded to the plane-stage width (1024): Xp rows hold xp_k_pad(K)/2 bytes, Xs rows xp_k_pad(K)/32
+int xp_k_pad(int K);
+// X bf16 [batch x ldx] -> Xp [8*batch x ldxp] packed e2m1 pieces, Xs [8*batch x ldxs] ue8m0 scales
+void xp_prep_launch(const void* X, int ldx, int K, int batch, uint8_t* Xp, int ldxp, uint8_t* Xs, int ldxs,
+                    cudaStream_t stream);
+CUtensorMap tmap_bits4(const uint8_t* bits, uint64_t rows, uint64_t cols);
+CUtensorMap tmap_xp(const uint8_t* Xp, int rows, int ldxp);
+CUtensorMap tmap_xs(const uint8_t* Xs, int rows, int ldxs);
+
 // ---- K3 byte-LUT (few requests per tenant; lut.cu) ----
 constexpr int kLutMaxSegs = 3;
 constexpr int kLutMaxChunks = 48;
