@@ -3,6 +3,7 @@
 // message for bd_last_error(); CUDA errors map to BD_ERR_CUDA.
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -101,7 +102,7 @@ void multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int32_
     // ---- K23: base GEMM + FP4 tensor-core deltas in one persistent kernel ----
     bool aligned16 = in_dim % 128 == 0 && out_dim % 128 == 0;
     for (int t : order) aligned16 &= (reinterpret_cast<uintptr_t>(tenant_bits[t]) % 16) == 0;
-    if ((mode == "mt4" || mode == "auto") && aligned16 && !order.empty() && batch <= 64) {
+    if ((mode == "mt4" || (mode == "auto" && max_per_tenant > 4)) && aligned16 && !order.empty() && batch <= 64) {
         Mt4Params prm{};
         prm.n_subs = 1;
         prm.sub_row0[0] = 0;
@@ -126,29 +127,51 @@ void multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int32_
             }
         }
         if (ok && plan_mt4(prm, out_dim, in_dim, batch)) {
-            const int kpad = xp_k_pad(int(in_dim));
-            const int ldxp = kpad / 2, ldxs = kpad / 32;
             const size_t sz_p = sizeof(float) * prm.splits * batch * out_dim;
-            const size_t sz_xp = size_t(8) * batch * ldxp, sz_xs = size_t(8) * batch * ldxs;
+            const size_t sz_xp = size_t(batch) * prm.n_chunks * kXpBlock;
             const size_t sz_m = maps.size() * sizeof(CUtensorMap);
+            const std::vector<uint32_t> sched = mt4_schedule(prm);
+            const size_t sz_s = sched.size() * sizeof(uint32_t);
             char* ws = nullptr;
-            BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), sz_p + sz_xp + sz_xs + sz_m + 1024, stream));
+            BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), sz_p + sz_xp + sz_m + sz_s + 1024, stream));
             char* cur = ws;
             auto take = [&](size_t n) { char* r = cur; cur += (n + 255) & ~size_t(255); return r; };
             float* P = reinterpret_cast<float*>(take(sz_p));
-            uint8_t* Xp = reinterpret_cast<uint8_t*>(take(sz_xp));
-            uint8_t* Xs = reinterpret_cast<uint8_t*>(take(sz_xs));
+            uint8_t* xpk = reinterpret_cast<uint8_t*>(take(sz_xp));
             CUtensorMap* dmaps = reinterpret_cast<CUtensorMap*>(take(sz_m));
+            uint32_t* dsched = reinterpret_cast<uint32_t*>(take(sz_s));
             BD_CUDA(cudaMemcpyAsync(dmaps, maps.data(), sz_m, cudaMemcpyHostToDevice, stream));
+            BD_CUDA(cudaMemcpyAsync(dsched, sched.data(), sz_s, cudaMemcpyHostToDevice, stream));
             BD_CUDA(cudaStreamSynchronize(stream));  // host staging consumed
             prm.map_w = mw;
             prm.map_x = tmap_acts(X, batch, in_dim, in_dim, prm.bn);
-            prm.map_xp = tmap_xp(Xp, 8 * batch, ldxp);
-            prm.map_xs = tmap_xs(Xs, 8 * batch, ldxs);
+            prm.xpk = xpk;
+            prm.sched = dsched;
             prm.bits_maps = dmaps;
             prm.partial = P;
-            xp_prep_launch(X, int(in_dim), int(in_dim), batch, Xp, ldxp, Xs, ldxs, stream);
+            xp_prep_launch(X, int(in_dim), int(in_dim), batch, xpk, stream);
+            static const bool tr = std::getenv("BD_MT4_TRACE") != nullptr;
+            if (tr) {
+                BD_CUDA(cudaMalloc(&prm.trace, 8 * 512 * sizeof(long long)));
+                BD_CUDA(cudaMemset(prm.trace, 0, 8 * 512 * sizeof(long long)));
+                mt4_launch(prm, stream);  // warm
+            }
             mt4_launch(prm, stream);
+            if (tr) {
+                std::vector<long long> h(8 * 512);
+                BD_CUDA(cudaMemcpyAsync(h.data(), prm.trace, h.size() * 8, cudaMemcpyDeviceToHost, stream));
+                BD_CUDA(cudaStreamSynchronize(stream));
+                const long long t0 = h[512];
+                fprintf(stderr, "stage: clock64 of the trace points (role 0..7) relative to the MMA warp's first full\n");
+                for (int i = 0; i < 512; ++i) {
+                    if (!h[512 + i]) break;
+                    fprintf(stderr, "%4d", i);
+                    for (int r = 0; r < 8; ++r) fprintf(stderr, " %8lld", h[r * 512 + i] ? h[r * 512 + i] - t0 : -1);
+                    fprintf(stderr, "\n");
+                }
+                BD_CUDA(cudaFree(prm.trace));
+                prm.trace = nullptr;
+            }
             combine_launch(P, prm.splits, nullptr, batch, int(out_dim), Y, stream);
             BD_CUDA(cudaFreeAsync(ws, stream));
             return;

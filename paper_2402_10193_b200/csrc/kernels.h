@@ -104,31 +104,38 @@ constexpr int kMt4MaxReq = 4;   // requests per slot (MMA N = 8 pieces x n_req <
 constexpr int kMt4MaxSubs = 3;
 struct Mt4Slot {
     int n_req;
-    int req[kMt4MaxReq];          // batch indices (Xp/Xs rows 8*req .. 8*req+7)
+    int req[kMt4MaxReq];          // batch indices (activation piece blocks of request req[q])
     float alpha[kMt4MaxSubs];     // per stacked sub-matrix
     int map_idx[kMt4MaxSubs];     // index into the bits tensor-map table
 };
 struct Mt4Params {
-    CUtensorMap map_w, map_x, map_xp, map_xs;
+    CUtensorMap map_w, map_x;
     const CUtensorMap* bits_maps;  // device table (tmap_bits4)
+    const uint8_t* xpk;            // FP4 activation pieces + scales, [batch][n_chunks][kXpBlock]
+    const uint32_t* sched;         // per-tile stage schedule (mt4_schedule), device memory
     float* partial;                // [splits][batch][M]
     long long total_stages;
     int M, K, batch, bn, nr_max, n_subs, n_slots;
     int sub_row0[kMt4MaxSubs + 1];
-    int kb_base, kc_plane, stages_per_tile, grid, splits, stages, smem;
+    int kb_base, kc_plane, stages_per_tile, grid, splits, ring_b, ring_p, smem, n_chunks;
+    int col_base, col_acc, acc_stride, n_acc, col_sfa, col_ring, n_ring;  // TMEM layout
+    int debug;  // experiment flags (BD_MT4_DEBUG), 0 in production
+    long long* trace;  // CTA 0 clock64 timeline (BD_MT4_TRACE), null in production
     Mt4Slot slots[kMt4MaxSlots];
 };
 // Fills the schedule (stages per tile, persistent grid, splits, smem ring); false if unsupported.
 bool plan_mt4(Mt4Params& p, uint64_t M, uint64_t K, int batch);
+// Host copy of the per-tile stage schedule for p (upload it and set p.sched).
+std::vector<uint32_t> mt4_schedule(const Mt4Params& p);
 void mt4_launch(const Mt4Params& p, cudaStream_t stream);
-// K padded to the plane-stage width (1024): Xp rows hold xp_k_pad(K)/2 bytes, Xs rows xp_k_pad(K)/32
-int xp_k_pad(int K);
-// X bf16 [batch x ldx] -> Xp [8*batch x ldxp] packed e2m1 pieces, Xs [8*batch x ldxs] ue8m0 scales
-void xp_prep_launch(const void* X, int ldx, int K, int batch, uint8_t* Xp, int ldxp, uint8_t* Xs, int ldxs,
-                    cudaStream_t stream);
+// Activation pieces, one contiguous block per (request, 1024-column chunk): 4 x [8 pieces x 128 B]
+// packed e2m1 (128-byte swizzled, K permuted inside 32-column blocks) + [8 x 32 B] ue8m0 scales.
+constexpr int kXpBlock = 4096 + 256;
+inline int xp_chunks(int K) { return (K + 1023) / 1024; }
+// X bf16 [batch x ldx] -> xpk [batch][xp_chunks(K)][kXpBlock]
+void xp_prep_launch(const void* X, int ldx, int K, int batch, uint8_t* xpk, cudaStream_t stream);
+// 2-D map of a sign plane (reference layout), box [128 rows x 128 B], 128-byte swizzle
 CUtensorMap tmap_bits4(const uint8_t* bits, uint64_t rows, uint64_t cols);
-CUtensorMap tmap_xp(const uint8_t* Xp, int rows, int ldxp);
-CUtensorMap tmap_xs(const uint8_t* Xs, int rows, int ldxs);
 
 // ---- K3 byte-LUT (few requests per tenant; lut.cu) ----
 constexpr int kLutMaxSegs = 3;

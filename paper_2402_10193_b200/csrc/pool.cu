@@ -133,6 +133,13 @@ struct Plan {
         LutParams prm;
     };
     std::vector<std::array<Lut, 4>> lut;
+    // K23 (base + FP4 tensor-core deltas in one kernel) per layer & group
+    struct M4 {
+        bool ok = false;
+        Mt4Params prm;
+    };
+    std::vector<std::array<M4, 4>> mt4;
+    uint8_t* xpk = nullptr;  // FP4 activation pieces + scales [B][chunks][kXpBlock]
     int8_t* Xq = nullptr;  // [256 x ldq] int8 pieces (zero padded)
     int ldq = 0;
     float* xscale = nullptr;
@@ -747,6 +754,110 @@ struct PoolImpl {
         }
     }
 
+    // K23 (mt4.cu): base GEMM + every tenant plane as FP4 MMAs in one persistent
+    // kernel. Slots are ordered by tenant id and, within a tenant, by request id,
+    // so the schedule (and every output bit) is independent of the batch order.
+    void plan_mt4_groups(Plan& p, std::map<int, std::vector<int>>& by_t) {
+        const int B = p.B;
+        const uint64_t nL = a.n_layers;
+        if (B > 64) return;
+        const int max_chunks = xp_chunks(int(std::max(a.dim, a.intermediate)));
+        std::vector<int> tids;
+        for (auto& kv : by_t) tids.push_back(kv.first);  // std::map: ascending tenant id
+        std::map<int, std::vector<int>> rq_sorted;
+        for (int t : tids) {
+            std::vector<int> rq = by_t[t];
+            std::sort(rq.begin(), rq.end(), [&](int x, int y) { return p.reqs[x] < p.reqs[y]; });
+            rq_sorted[t] = rq;
+        }
+        struct GroupDef {
+            std::vector<int> projs;
+            uint64_t cols;
+            const CUtensorMap* mx;
+        };
+        const GroupDef defs[4] = {{{P_Q, P_K, P_V}, a.dim, &p.x_xn},
+                                  {{P_O}, a.dim, &p.x_ctx},
+                                  {{P_GATE, P_UP}, a.dim, &p.x_xn},
+                                  {{P_DOWN}, a.intermediate, &p.x_act}};
+        bool any = false;
+        p.mt4.assign(nL, {});
+        for (int gi = 0; gi < 4; ++gi) {
+            const GroupDef& gd = defs[gi];
+            if (gd.cols % 128) continue;
+            bool ok = true;
+            uint64_t M = 0;
+            std::vector<int> sub_row0;
+            for (int pj : gd.projs) {
+                uint64_t r0, nr;
+                local_rows(pj, r0, nr);
+                if (nr % 128) ok = false;
+                sub_row0.push_back(int(M));
+                M += nr;
+            }
+            sub_row0.push_back(int(M));
+            if (!ok) continue;
+            for (uint64_t l = 0; l < nL && ok; ++l) {
+                Mt4Params prm{};
+                prm.n_subs = int(gd.projs.size());
+                for (size_t s2 = 0; s2 < sub_row0.size(); ++s2) prm.sub_row0[s2] = sub_row0[s2];
+                std::vector<CUtensorMap> maps;
+                for (int t : tids) {
+                    const auto& rq = rq_sorted[t];
+                    const size_t n_planes = tenants[t].proj[l][gd.projs[0]].size();
+                    for (size_t k = 0; k < n_planes && ok; ++k) {
+                        int midx[kMt4MaxSubs];
+                        for (size_t s2 = 0; s2 < gd.projs.size(); ++s2) {
+                            const int pj = gd.projs[s2];
+                            const auto& planes = tenants[t].proj[l][pj];
+                            if (planes.size() != n_planes ||
+                                reinterpret_cast<uintptr_t>(planes[k].bits) % 16) { ok = false; break; }
+                            uint64_t r0, nr;
+                            local_rows(pj, r0, nr);
+                            midx[s2] = int(maps.size());
+                            maps.push_back(tmap_bits4(planes[k].bits, nr, gd.cols));
+                        }
+                        for (size_t c = 0; c < rq.size() && ok; c += kMt4MaxReq) {
+                            if (prm.n_slots >= kMt4MaxSlots) { ok = false; break; }
+                            Mt4Slot& sl = prm.slots[prm.n_slots++];
+                            sl.n_req = int(std::min<size_t>(kMt4MaxReq, rq.size() - c));
+                            for (int q = 0; q < sl.n_req; ++q) sl.req[q] = rq[c + q];
+                            for (size_t s2 = 0; s2 < gd.projs.size(); ++s2) {
+                                sl.alpha[s2] = tenants[t].proj[l][gd.projs[s2]][k].alpha;
+                                sl.map_idx[s2] = midx[s2];
+                            }
+                        }
+                    }
+                }
+                if (!ok || !plan_mt4(prm, M, gd.cols, B)) { ok = false; break; }
+                if (uint64_t(prm.splits) * B * M > P_elems) { ok = false; break; }
+                if (!p.xpk) {
+                    p.xpk = dmalloc<uint8_t>(size_t(B) * max_chunks * kXpBlock, &p.allocs);
+                    BD_CUDA(cudaMemset(p.xpk, 0, size_t(B) * max_chunks * kXpBlock));
+                }
+                CUtensorMap* dm = dmalloc<CUtensorMap>(maps.size(), &p.allocs);
+                BD_CUDA(cudaMemcpy(dm, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+                prm.bits_maps = dm;
+                const std::vector<uint32_t> sched = mt4_schedule(prm);
+                uint32_t* dsch = dmalloc<uint32_t>(sched.size(), &p.allocs);
+                BD_CUDA(cudaMemcpy(dsch, sched.data(), sched.size() * 4, cudaMemcpyHostToDevice));
+                prm.sched = dsch;
+                const LayerW& W = L[l];
+                prm.map_w = gi == 0 ? W.m_qkv : gi == 1 ? W.m_o : gi == 2 ? W.m_gu : W.m_down;
+                const uint64_t ldx = gi == 3 ? ld_inter : ld_dim;
+                const uint16_t* X = gi == 1 ? ctx : gi == 3 ? act : xn;
+                prm.map_x = tmap_acts(X, B, gd.cols, ldx, prm.bn);
+                prm.xpk = p.xpk;
+                prm.partial = P;
+                p.mt4[l][gi].prm = prm;
+                p.mt4[l][gi].ok = true;
+                any = true;
+            }
+            if (!ok)
+                for (uint64_t l = 0; l < nL; ++l) p.mt4[l][gi].ok = false;
+        }
+        (void)any;
+    }
+
     // Tensor-core delta path (mtfused.cu) for every projection group whose
     // shapes allow it (plane rows start on 16-byte TMA boundaries: cols % 128,
     // stacked sub-matrix boundaries % 128) and whose slots fit TMEM.
@@ -791,6 +902,7 @@ struct PoolImpl {
             const GroupDef& gd = defs[gi];
             if (gd.cols % 128) continue;
             if (!p.lut.empty() && p.lut[0][gi].ok) continue;  // LUT path already chosen
+            if (!p.mt4.empty() && p.mt4[0][gi].ok) continue;  // K23 already chosen
             bool ok = true;
             uint64_t M = 0;
             std::vector<int> sub_row0;
@@ -969,7 +1081,14 @@ struct PoolImpl {
         p->x_act = tmap_acts(act, B, a.intermediate, ld_inter, bn);
         size_t max_per_tenant = 0;
         for (int t : order) max_per_tenant = std::max(max_per_tenant, by_t[t].size());
+        // K23 (mt4) when forced, or by default for tenants with many requests each
+        // (the byte-LUT beside K2 is measured faster at one request per tenant)
+        if (delta_mode == "mt4" || (delta_mode == "auto" && max_per_tenant > 4)) plan_mt4_groups(*p, by_t);
         if (delta_mode == "lut" || (delta_mode == "auto" && max_per_tenant <= 4)) plan_lut_groups(*p);
+        // groups already served by K23 keep neither LUT nor fused plans
+        for (uint64_t l = 0; l < p->mt4.size(); ++l)
+            for (int gi = 0; gi < 4; ++gi)
+                if (p->mt4[l][gi].ok && !p->lut.empty()) p->lut[l][gi].ok = false;
         if (concurrent_k23 && !p->lut.empty()) {
             // K2 runs beside the K3 LUT on every SM: one GEMM CTA per SM within the
             // shared memory the LUT leaves (LUT: 132 KB + 512 threads x 96 regs)
@@ -1022,7 +1141,18 @@ struct PoolImpl {
         return p.fused.size() > l && p.fused[l][gi].ok;
     }
     bool lut_ok(const Plan& p, uint64_t l, int gi) const { return p.lut.size() > l && p.lut[l][gi].ok; }
+    bool mt4_ok(const Plan& p, uint64_t l, int gi) const { return p.mt4.size() > l && p.mt4[l][gi].ok; }
     ProjOut group_out(const Plan& p, uint64_t l, int gi, const GemmPlan& g) const {
+        if (mt4_ok(p, l, gi)) {
+            const Mt4Params& f = p.mt4[l][gi].prm;
+            ProjOut o;
+            o.P = P;
+            o.splits = f.splits;
+            o.pstride = size_t(p.B) * f.M;
+            o.D = nullptr;
+            o.M = f.M;
+            return o;
+        }
         if (lut_ok(p, l, gi)) {
             ProjOut o = proj_out(g, true);
             o.dsplits = p.lut[l][gi].prm.slices;
@@ -1044,6 +1174,11 @@ struct PoolImpl {
     void linear(Plan& p, uint64_t l, int group, const GemmPlan& g, const CUtensorMap& mw,
                 const CUtensorMap& mx, const std::vector<DeltaUnit>& units, const uint16_t* X,
                 int ldx, int cols, int B, cudaStream_t s) {
+        if (mt4_ok(p, l, group)) {
+            prof(BD_PROF_XQ_PREP, s, [&] { xp_prep_launch(X, ldx, cols, B, p.xpk, s); });
+            prof(BD_PROF_FUSED_QKV + group, s, [&] { mt4_launch(p.mt4[l][group].prm, s); });
+            return;
+        }
         if (lut_ok(p, l, group)) {
             if (concurrent_k23) {
                 // K3 (CUDA cores / LSU) and K2 (TMA + tensor pipe) share every SM:

@@ -188,10 +188,7 @@ def test_multitenant_linear(cuda, rows, cols, B, T):
     assert rel_l2(Y.cpu().numpy(), want.cpu().numpy()) <= 1e-5
 
 
-@pytest.mark.parametrize("rows,cols,B,T", [(4096, 4096, 16, 16), (1024, 11008, 8, 3), (512, 1024, 1, 1)])
-def test_multitenant_linear_delta_only(cuda, rows, cols, B, T):
-    """Zero backbone: Y is the delta term alone, so its error is not diluted by the base
-    product. FP4 activation pieces (K23) and the LUT both stay within 1e-5 rel-L2 of f64."""
+def _delta_only_case(rows, cols, B, T, cuda):
     torch.manual_seed(7 + rows)
     W = torch.zeros(rows, cols, device=cuda, dtype=torch.bfloat16)
     # activations with a wide dynamic range inside each 32-column block
@@ -204,7 +201,36 @@ def test_multitenant_linear_delta_only(cuda, rows, cols, B, T):
     rt = [b % T for b in range(B)]
     Y = bd.multitenant_linear(W, bits_list, alphas, rt, X)
     want = _mt_reference(W, bits_list, alphas, rt, X, rows, cols)
-    assert rel_l2(Y.cpu().numpy(), want.cpu().numpy()) <= 1e-5
+    return rel_l2(Y.cpu().numpy(), want.cpu().numpy())
+
+
+@pytest.mark.parametrize("rows,cols,B,T", [(4096, 4096, 16, 16), (1024, 11008, 8, 3), (512, 1024, 1, 1)])
+def test_multitenant_linear_delta_only(cuda, rows, cols, B, T):
+    """Zero backbone: Y is the delta term alone, so its error is not diluted by the base
+    product (default path) — within 1e-5 rel-L2 of f64."""
+    assert _delta_only_case(rows, cols, B, T, cuda) <= 1e-5
+
+
+@pytest.mark.parametrize("mode", ["mt4", "lut"])
+def test_multitenant_linear_delta_only_each_path(cuda, mode):
+    """Delta term alone through K23 (FP4 pieces, ~1e-7 measured) and the byte LUT."""
+    import subprocess
+    import sys
+
+    code = f"""
+import sys; sys.path.insert(0, {repr(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))})
+sys.path.insert(0, {repr(os.path.dirname(os.path.abspath(__file__)))})
+import torch
+from test_gpu_kernels import _delta_only_case
+dev = torch.device('cuda:0')
+for case in [(4096, 4096, 16, 16), (1024, 11008, 8, 3), (512, 1024, 1, 1), (1024, 4096, 64, 4)]:
+    err = _delta_only_case(*case, dev)
+    assert err <= 1e-5, (case, err)
+print('ok')
+"""
+    env = dict(os.environ, BD_DELTA=mode)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
 def test_multitenant_linear_permutation_bit_identical(cuda):
