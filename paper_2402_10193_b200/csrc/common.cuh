@@ -8,7 +8,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <string>
+#include <utility>
 
 #include "../../include/bitdelta/capi.h"
 
@@ -278,6 +280,16 @@ __device__ __forceinline__ void mbar_arrive_cnt_w(uint64_t* bar, uint32_t count)
         "@e mbarrier.arrive.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(smem_u32(bar)), "r"(count)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_x_w(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                                int32_t c1) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];\n\t}" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_2d_w(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
                                               int32_t c1, uint64_t policy) {
     asm volatile(
@@ -299,6 +311,34 @@ __device__ __forceinline__ void bulk_load_w(void* smem_dst, const void* src, uin
             smem_u32(smem_dst)),
         "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
+}
+
+// ---- programmatic dependent launch (PDL) ----
+// Kernels of the decode step are launched with programmatic stream serialization:
+// a kernel's CTAs may be scheduled while its predecessor drains, and wait here
+// (griddepcontrol.wait: the predecessor grid has completed and its writes are
+// visible) before touching anything the predecessor produced. A no-op when the
+// kernel was launched without the attribute.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+    static const bool on = !(std::getenv("BD_PDL") && std::getenv("BD_PDL")[0] == '0');
+    return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }

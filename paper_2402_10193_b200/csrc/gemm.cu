@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t taddr = *tmem_slot;
+    griddep_wait();  // PDL: the activations come from the previous kernel
 
     if (warp == 0 && lane == 0) {
         // ---- TMA producer ----
@@ -255,8 +256,8 @@ void base_gemm_launch(const GemmPlan& p, const CUtensorMap& map_w, const CUtenso
         attr_set = true;
     }
     dim3 grid(p.m_tiles, p.splits);
-    base_gemm_kernel<<<grid, kGemmThreads, p.smem, stream>>>(
-        map_w, map_x, partial, int(p.M), p.batch, p.bn, p.kb_total, p.kb_per_split, p.stages);
+    BD_CUDA(launch_pdl(base_gemm_kernel, grid, dim3(kGemmThreads), size_t(p.smem), stream, map_w, map_x, partial,
+                       int(p.M), p.batch, p.bn, p.kb_total, p.kb_per_split, p.stages));
     note_launch();
     BD_CUDA(cudaGetLastError());
 }

@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(kRnThreads)
                       unsigned* __restrict__ arrive, double* __restrict__ msq_part) {
     __shared__ double red_d[32];
     __shared__ double inv_s;
+    griddep_wait();  // PDL: the projection partials come from the previous kernel
     const int b = blockIdx.y, nc = gridDim.x;
     const int i = blockIdx.x * kRnChunk + 4 * threadIdx.x;
     const bool on = i < dim;
@@ -465,6 +466,7 @@ __global__ void __launch_bounds__(kA2Threads)
     uint16_t* st = reinterpret_cast<uint16_t*>(vs + hd);            // [stage_rows_max][hd]: K, then V, then partials
     float* scores = reinterpret_cast<float*>(st + stage_rows_max * hd);  // max_seq
     __shared__ float red[32];
+    griddep_wait();  // PDL: q/k/v partials come from the previous kernel
     const int h = blockIdx.x, b = blockIdx.y;
     const int group = a.n_heads / a.n_kv_heads;
     const int kh = h / group;
@@ -597,6 +599,7 @@ __global__ void silu_kernel(ProjOut gu, int inter, uint16_t* __restrict__ act, i
 }
 // 4 outputs per thread (aligned shapes), same per-element arithmetic
 __global__ void silu4_kernel(ProjOut gu, int inter, uint16_t* __restrict__ act, int ld_act) {
+    griddep_wait();  // PDL: gate/up partials come from the previous kernel
     const int b = blockIdx.y;
     for (int i = 4 * (blockIdx.x * blockDim.x + threadIdx.x); i < inter; i += 4 * gridDim.x * blockDim.x) {
         const float4 g = proj_val4(gu, b, i);
@@ -702,8 +705,8 @@ void resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const 
     static const bool two_phase = std::getenv("BD_NORM_TWO") && std::getenv("BD_NORM_TWO")[0] == '1';
     if (!two_phase && dim % 4 == 0 && ldxn % 4 == 0 && proj_vec4_ok(proj) &&
         size_t(nc) * batch <= size_t(kNumSMs) * 8) {
-        resid_norm_kernel<<<dim3(nc, batch), kRnThreads, 0, s>>>(x, dim, proj, norm_w, xn, ldxn, xn_f32,
-                                                                   arrive, msq_ws);
+        BD_CUDA(launch_pdl(resid_norm_kernel, dim3(nc, batch), dim3(kRnThreads), 0, s, x, dim, proj, norm_w, xn,
+                           ldxn, xn_f32, arrive, msq_ws));
         note_launch();
         BD_CUDA(cudaGetLastError());
         return;
@@ -741,7 +744,8 @@ void attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int 
             attr2 = true;
         }
         require(smem <= 220 * 1024, BD_ERR_BAD_ARGUMENT, "attention: max_seq too large for the score buffer");
-        attn128_kernel<<<dim3(a.n_heads, batch), kA2Threads, smem, s>>>(qkv, a, pos_dev, ctx, ld_ctx, rows);
+        BD_CUDA(launch_pdl(attn128_kernel, dim3(a.n_heads, batch), dim3(kA2Threads), smem, s, qkv, a, pos_dev, ctx,
+                           ld_ctx, rows));
         note_launch();
         BD_CUDA(cudaGetLastError());
         return;
@@ -761,7 +765,7 @@ void attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int 
 void silu_launch(const ProjOut& gu, int batch, int inter, uint16_t* act, int ld_act, cudaStream_t s) {
     if (inter % 4 == 0 && ld_act % 4 == 0 && proj_vec4_ok(gu)) {
         const int bx = std::max(1, std::min((inter / 4 + 127) / 128, 64));
-        silu4_kernel<<<dim3(bx, batch), 128, 0, s>>>(gu, inter, act, ld_act);
+        BD_CUDA(launch_pdl(silu4_kernel, dim3(bx, batch), dim3(128), 0, s, gu, inter, act, ld_act));
     } else {
         const int bx = std::max(1, std::min((inter + 255) / 256, 64));
         silu_kernel<<<dim3(bx, batch), 256, 0, s>>>(gu, inter, act, ld_act);

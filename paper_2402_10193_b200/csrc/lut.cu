@@ -75,6 +75,7 @@ __global__ void __maxnreg__(kLutRegs)
                float* __restrict__ out) {
     extern __shared__ float T[];
     __shared__ float xs[32 * 33];  // x of the slice, [lane][32 columns] padded to 33
+    griddep_wait();  // PDL: X comes from the previous kernel; D is still read by it
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int kWarps = kLutThreads / 32;
     const uint32_t lb0 = 4u * lane, lb1 = 4u * lane + 128u;  // low byte of the entry offset
@@ -211,7 +212,8 @@ void lut_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t st
                                          int(cudaSharedmemCarveoutMaxShared)));
         attr = true;
     }
-    lut_kernel<kWPR><<<p.grid, kLutThreads, kTableBytes, stream>>>(p, static_cast<const uint16_t*>(X), out);
+    BD_CUDA(launch_pdl(lut_kernel<kWPR>, dim3(p.grid), dim3(kLutThreads), kTableBytes, stream, p,
+                       static_cast<const uint16_t*>(X), out));
 }
 
 void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream) {

@@ -245,6 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1) mt4_kernel(const __grid_constant_
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
+    griddep_wait();  // PDL: activations come from the previous kernels
 
     if (warp == 0 || warp == 2 || warp == 3) {
         // ---- TMA producers: three warps take stages round-robin (the copies one
@@ -526,6 +527,7 @@ __device__ __forceinline__ float e2m1_value(uint32_t c) {
 __global__ void __launch_bounds__(256) xp_prep_kernel(const uint16_t* __restrict__ X, int ldx, int K, int n_chunks,
                                                        uint8_t* __restrict__ xpk) {
     __shared__ uint32_t nib[8][32];
+    griddep_wait();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int b = blockIdx.y;
     const int u = blockIdx.x * 8 + warp;  // 32-column block
@@ -675,15 +677,15 @@ void mt4_launch(const Mt4Params& p, cudaStream_t stream) {
         BD_CUDA(cudaFuncSetAttribute(mt4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr = true;
     }
-    mt4_kernel<<<p.grid, kThreads, p.smem, stream>>>(p);
+    BD_CUDA(launch_pdl(mt4_kernel, dim3(p.grid), dim3(kThreads), size_t(p.smem), stream, p));
     note_launch();
     BD_CUDA(cudaGetLastError());
 }
 
 void xp_prep_launch(const void* X, int ldx, int K, int batch, uint8_t* xpk, cudaStream_t stream) {
     const int n_chunks = xp_chunks(K);
-    xp_prep_kernel<<<dim3(n_chunks * 4, batch), 256, 0, stream>>>(static_cast<const uint16_t*>(X), ldx, K, n_chunks,
-                                                                  xpk);
+    BD_CUDA(launch_pdl(xp_prep_kernel, dim3(n_chunks * 4, batch), dim3(256), 0, stream,
+                       static_cast<const uint16_t*>(X), ldx, K, n_chunks, xpk));
     note_launch();
     BD_CUDA(cudaGetLastError());
 }

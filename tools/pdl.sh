@@ -1,0 +1,6 @@
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+for pdl in 1 0 1; do
+BD_PDL=$pdl timeout 300 python bench.py --steps 50 --warmup 5 --no-cpu-baseline > gpurun_out/v.json 2>gpurun_out/v.err
+python -c "
+import json;d=json.load(open('gpurun_out/v.json'));print('pdl=$pdl', d['value'], d['ms_per_step'])" 2>/dev/null || tail -2 gpurun_out/v.err
+done
