@@ -19,18 +19,18 @@ __device__ __forceinline__ void mma_mxf4_ts(uint32_t d, uint32_t a, uint64_t bde
 }
 
 __global__ void probe(int N, int kb, int mode, int sfid, float* D) {
-  __shared__ __align__(1024) uint8_t bs[32 * 128];
+  __shared__ __align__(1024) uint8_t bs[128 * 128];
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
   int t = threadIdx.x, w = t >> 5, l = t & 31;
-  for (int i = t; i < 32 * 128; i += 128) bs[i] = 0;
+  for (int i = t; i < 128 * 128; i += 128) bs[i] = 0;
   __syncthreads();
   for (int i = t; i < N * 32; i += 128) {
     int r = i / 32, byte = i % 32, chunk = byte / 16;
     int phys = ((chunk ^ (r & 7)) * 16) + byte % 16;
     bs[r * 128 + phys] = (byte / 16 == kb) ? 0x22 : 0x00;  // block kb = bytes [16kb, 16kb+16)
   }
-  if (w == 0) tmem_alloc<128>(&slot);
+  if (w == 0) tmem_alloc<256>(&slot);
   if (t == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
   tc_fence_before(); __syncthreads(); tc_fence_after();
   uint32_t tb = slot, lane_base = (w * 32) << 16;
@@ -48,32 +48,34 @@ __global__ void probe(int N, int kb, int mode, int sfid, float* D) {
     b[c] = v;
   }
   tmem_st8(tb + lane_base + 72, b);   // B scales: cols 72..79
-  tmem_st8(tb + lane_base + 32, z);
+  for (int c0 = 0; c0 < 128; c0 += 8) tmem_st8(tb + lane_base + 128 + c0, z);
   tmem_st_wait();
   fence_proxy_async();
   tc_fence_before(); __syncthreads(); tc_fence_after();
   if (t == 0) {
     uint32_t idesc = (uint32_t(sfid) << 4) | (1u << 7) | (1u << 10) | ((uint32_t(N) >> 3) << 17) | (1u << 23) |
                      ((128u >> 4) << 24);
-    mma_mxf4_ts(tb + 32, tb + 0, sdesc_k128(bs), idesc, tb + 64, tb + 72, 0);
+    mma_mxf4_ts(tb + 128, tb + 0, sdesc_k128(bs), idesc, tb + 64, tb + 72, 0);
     tc_commit(&bar);
   }
   mbar_wait(&bar, 0);
   tc_fence_after();
-  uint32_t v[16];
-  tmem_ld16(tb + lane_base + 32, v);
-  tmem_ld_wait();
-  for (int n = 0; n < N; ++n) D[t * N + n] = __uint_as_float(v[n]);
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    uint32_t v[16];
+    tmem_ld16(tb + lane_base + 128 + c0, v);
+    tmem_ld_wait();
+    for (int n = 0; n < 16 && c0 + n < N; ++n) D[t * N + c0 + n] = __uint_as_float(v[n]);
+  }
   tc_fence_before(); __syncthreads();
-  if (w == 0) tmem_dealloc<128>(tb);
+  if (w == 0) tmem_dealloc<256>(tb);
 }
 
 int main() {
-  float* dD; cudaMalloc(&dD, 128 * 16 * 4);
-  std::vector<float> D(128 * 16);
-  for (int sfid : {0, 2})
-  for (int N : {8, 16}) for (int kb : {0, 1}) {
-    int codes[2][16];
+  float* dD; cudaMalloc(&dD, 128 * 128 * 4);
+  std::vector<float> D(128 * 128);
+  for (int sfid : {0})
+  for (int N : {64, 128}) for (int kb : {0}) {
+    int codes[2][128];
     for (int mode : {0, 1}) {
       probe<<<1, 128>>>(N, kb, mode, sfid, dD);
       cudaError_t e = cudaDeviceSynchronize();
@@ -89,7 +91,7 @@ int main() {
     printf("sfid=%d N=%2d kb=%d: ", sfid, N, kb);
     for (int n = 0; n < N; ++n) {
       int c1 = codes[1][n];
-      printf("n%d[l%d c%d b%d] ", n, codes[0][n], c1 / 4, c1 % 4);
+      if (n % 8 == 0 || n == 31 || n == 32 || n == 33) printf("n%d[l%d c%d b%d] ", n, codes[0][n], c1 / 4, c1 % 4);
     }
     printf("\n");
   }
