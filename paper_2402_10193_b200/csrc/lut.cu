@@ -30,9 +30,15 @@ void note_launch();
 
 namespace {
 
-constexpr int kLutThreads = 512;
+#ifndef BD_LUT_THREADS
+#define BD_LUT_THREADS 512
+#endif
+#ifndef BD_LUT_REGS
+#define BD_LUT_REGS 96
+#endif
+constexpr int kLutThreads = BD_LUT_THREADS;
 // <= 96 registers so a base-GEMM CTA (128 threads) can be co-resident on the SM
-constexpr int kLutRegs = 96;
+constexpr int kLutRegs = BD_LUT_REGS;
 constexpr int kSliceCols = 1024;
 constexpr size_t kTableBytes = 4 * 256 * 32 * sizeof(float);  // 128 KB
 constexpr int R = 16;                                          // rows per warp batch
@@ -98,7 +104,7 @@ __global__ void __maxnreg__(kLutRegs)
             for (int i = threadIdx.x; i < kSliceCols; i += kLutThreads)
                 xs[(i >> 5) * 33 + (i & 31)] = (c0 + i < p.cols) ? bf16_to_f32(xr[c0 + i]) : 0.0f;
             __syncthreads();
-            if (!(p.debug & 1)) build_tables(T, xs);
+            if (!(p.debug & 1) && threadIdx.x < 512) build_tables(T, xs);  // 512 builders: 128 tables x 4 quarters
             __syncthreads();
             cur = u;
         }
