@@ -157,6 +157,10 @@ struct LutParams {
 bool plan_lut(LutParams& p, const int* seg_rows, int n_segs, int cols, int ldx, int batch);
 // out: [slices][batch][M] f32, alpha already applied; every (slice, req, row) of a job written
 void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream);
+// K3b (bmma.cu): same plan and output as the LUT on the binary tensor-core path
+// (cols % 128 == 0, 16-byte aligned planes; BD_LUT_B1=0 disables)
+bool b1_supported(const LutParams& p);
+void b1_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream);
 
 // Y[b][m] = sum_s P[s][b][m] (+ D[b][m])
 void combine_launch(const float* P, int splits, const float* D, int batch, int M, float* Y,

@@ -223,6 +223,10 @@ void lut_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t st
 }
 
 void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream) {
+    if (b1_supported(p)) {
+        b1_launch(p, X, out, stream);
+        return;
+    }
     // compile-time row strides for the published shapes (immediate load offsets)
     switch (p.cols) {
         case 4096: lut_launch_t<128>(p, X, out, stream); break;

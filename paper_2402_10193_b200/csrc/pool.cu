@@ -1093,9 +1093,12 @@ struct PoolImpl {
             // K2 runs beside the K3 LUT on every SM: one GEMM CTA per SM within the
             // shared memory the LUT leaves (LUT: 132 KB + 512 threads x 96 regs)
             GemmPlan* gs[4] = {&p->g_qkv, &p->g_o, &p->g_gu, &p->g_down};
+            // (the opt-in binary tensor-core K3b needs only 3.3 KB of shared memory: K2 takes the rest)
+            static const int b1_cap = 190;
             for (int gi = 0; gi < 4; ++gi)
                 if (p->lut[0][gi].ok) {
-                    *gs[gi] = plan_base_gemm(gs[gi]->M, gs[gi]->K, B, 88 * 1024);
+                    const int cap = b1_supported(p->lut[0][gi].prm) ? b1_cap * 1024 : 88 * 1024;
+                    *gs[gi] = plan_base_gemm(gs[gi]->M, gs[gi]->K, B, cap);
                     require(uint64_t(gs[gi]->splits) * B * gs[gi]->M <= P_elems, BD_ERR_CUDA,
                             "split-K workspace too small");
                 }
