@@ -202,6 +202,8 @@ def run_ours(args, rank, world, dev):
 
     wl = WORKLOADS[args.workload]
     arch = dict(wl["arch"], rope_theta=10000.0)
+    if os.environ.get("BD_BENCH_INTER"):  # shape experiments only (not a BASELINE config)
+        arch["intermediate"] = int(os.environ["BD_BENCH_INTER"])
     T = args.tenants or wl["tenants"]
     B = args.batch or wl["batch"]
     ctx = args.ctx or wl["ctx"]

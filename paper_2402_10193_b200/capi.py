@@ -11,7 +11,7 @@ import os
 from functools import lru_cache
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbitdelta_b200.so")
+LIB_PATH = os.environ.get("BD_LIB") or os.path.join(HERE, "libbitdelta_b200.so")  # BD_LIB: A/B experiments
 
 u64 = C.c_uint64
 vp = C.c_void_p

@@ -32,7 +32,8 @@ __device__ __forceinline__ const float* proj_ptr(const ProjOut& p, int k, int b,
 __device__ __forceinline__ int proj_parts(const ProjOut& p) { return p.splits + (p.D ? p.dsplits : 0); }
 
 // All partial loads are issued before the (fixed-order) additions: the reduction
-// costs one memory latency instead of one per partial.
+// costs one memory latency per group of partials instead of one per partial.
+constexpr int kPartGroup = 16;  // float4 paths (norm: 128 threads, one float4 each)
 __device__ __forceinline__ float proj_val(const ProjOut& p, int b, int m) {
     if (p.G) {
         const int r = m / p.g_cols, i = m - r * p.g_cols;
@@ -40,7 +41,7 @@ __device__ __forceinline__ float proj_val(const ProjOut& p, int b, int m) {
     }
     const int n = proj_parts(p);
     float s = 0.0f;
-    for (int k0 = 0; k0 < n; k0 += 8) {
+    for (int k0 = 0; k0 < n; k0 += 8) {  // 8: register budget of the 4-CTA/SM attention kernel
         float t[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) t[j] = (k0 + j < n) ? *proj_ptr(p, k0 + j, b, m) : 0.0f;
@@ -50,7 +51,6 @@ __device__ __forceinline__ float proj_val(const ProjOut& p, int b, int m) {
     }
     return s;
 }
-
 __device__ __forceinline__ uint16_t f32_to_bf16(float v) {
     return __bfloat16_as_ushort(__float2bfloat16_rn(v));
 }
@@ -134,17 +134,45 @@ __device__ __forceinline__ float4 proj_val4(const ProjOut& p, int b, int m) {
     }
     const int n = proj_parts(p);
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int k0 = 0; k0 < n; k0 += 8) {
-        float4 t[8];
+    for (int k0 = 0; k0 < n; k0 += kPartGroup) {
+        float4 t[kPartGroup];
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < kPartGroup; ++j)
             t[j] = (k0 + j < n) ? *reinterpret_cast<const float4*>(proj_ptr(p, k0 + j, b, m))
                                 : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < kPartGroup; ++j)
             if (k0 + j < n) s = f4_add(s, t[j]);
     }
     return s;
+}
+// gate and up (same projection, columns m and m + off) with both load sets in flight
+__device__ __forceinline__ void proj_val4_pair(const ProjOut& p, int b, int m, int off, float4& g, float4& u) {
+    if (p.G) {
+        g = proj_val4(p, b, m);
+        u = proj_val4(p, b, m + off);
+        return;
+    }
+    constexpr int kG = kPartGroup / 2;
+    const int n = proj_parts(p);
+    g = make_float4(0.f, 0.f, 0.f, 0.f);
+    u = g;
+    for (int k0 = 0; k0 < n; k0 += kG) {
+        float4 tg[kG], tu[kG];
+#pragma unroll
+        for (int j = 0; j < kG; ++j) {
+            const bool on = k0 + j < n;
+            tg[j] = on ? *reinterpret_cast<const float4*>(proj_ptr(p, k0 + j, b, m)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            tu[j] = on ? *reinterpret_cast<const float4*>(proj_ptr(p, k0 + j, b, m + off))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int j = 0; j < kG; ++j)
+            if (k0 + j < n) {
+                g = f4_add(g, tg[j]);
+                u = f4_add(u, tu[j]);
+            }
+    }
 }
 
 __global__ void __launch_bounds__(kRnThreads)
@@ -167,6 +195,8 @@ __global__ void __launch_bounds__(kRnThreads)
         }
     }
     if (!norm_w) return;
+    // the tenant's norm row does not depend on the arrival: load it before the sync
+    const float4 w = on ? *reinterpret_cast<const float4*>(norm_w[b] + i) : make_float4(0.f, 0.f, 0.f, 0.f);
     double sq = static_cast<double>(v.x) * v.x + static_cast<double>(v.y) * v.y +
                 static_cast<double>(v.z) * v.z + static_cast<double>(v.w) * v.w;
     sq = block_sum(sq, red_d);
@@ -184,7 +214,6 @@ __global__ void __launch_bounds__(kRnThreads)
     __syncthreads();
     if (!on) return;
     const double inv = inv_s;
-    const float4 w = *reinterpret_cast<const float4*>(norm_w[b] + i);
     const float y0 = static_cast<float>(static_cast<double>(v.x) * inv) * w.x;
     const float y1 = static_cast<float>(static_cast<double>(v.y) * inv) * w.y;
     const float y2 = static_cast<float>(static_cast<double>(v.z) * inv) * w.z;
@@ -602,8 +631,8 @@ __global__ void silu4_kernel(ProjOut gu, int inter, uint16_t* __restrict__ act, 
     griddep_wait();  // PDL: gate/up partials come from the previous kernel
     const int b = blockIdx.y;
     for (int i = 4 * (blockIdx.x * blockDim.x + threadIdx.x); i < inter; i += 4 * gridDim.x * blockDim.x) {
-        const float4 g = proj_val4(gu, b, i);
-        const float4 u = proj_val4(gu, b, inter + i);
+        float4 g, u;
+        proj_val4_pair(gu, b, i, inter, g, u);
         auto f = [](float gv, float uv) { return f32_to_bf16(gv / (1.0f + expf(-gv)) * uv); };
         uint2 pk;
         pk.x = uint32_t(f(g.x, u.x)) | (uint32_t(f(g.y, u.y)) << 16);
