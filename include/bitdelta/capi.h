@@ -63,6 +63,14 @@ int bd_device_check(int device);
 /* Number of kernel launches this library issued since load (all streams). */
 uint64_t bd_launch_count(void);
 
+/* Diagnostics (no reference counterpart): device timeline of the decode-step kernels.
+ * bd_trace_enable(cap) allocates room for cap records (0 disables); every CTA of the
+ * K2/K3/glue kernels then appends {kind, cta, smid, pad, t_entry, t_wait, t_end}
+ * (u32 x4 + u64 x3, %globaltimer ns). bd_trace_read copies up to cap records and
+ * resets the count. */
+int bd_trace_enable(uint32_t capacity);
+int bd_trace_read(void* out, uint32_t capacity, uint32_t* n_out);
+
 /* ------------------------------------------------------------------ K1 -- */
 /* Replaces deltakit::compress_tensor (P:include/deltakit/delta.hpp:48,
  * P:src/delta.cpp:31-34) and, with base == NULL, compress_delta

@@ -7,6 +7,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
+#include <set>
 #include <vector>
 
 #include "common.cuh"
@@ -28,6 +30,35 @@ void cuda_check(cudaError_t e, const char* what) {
         throw Failure{BD_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
 }
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+namespace {
+std::mutex g_pdl_mu;
+std::set<const void*>& pdl_set() {
+    static std::set<const void*> s;
+    return s;
+}
+}  // namespace
+std::vector<TraceBinder>& trace_binders() {
+    static std::vector<TraceBinder> v;
+    return v;
+}
+int trace_register(TraceBinder b) {
+    trace_binders().push_back(b);
+    return 0;
+}
+namespace {
+TraceRec* g_tr_buf = nullptr;
+unsigned* g_tr_cnt = nullptr;
+unsigned g_tr_cap = 0;
+}  // namespace
+void note_pdl_kernel(const void* fn) {
+    std::lock_guard<std::mutex> g(g_pdl_mu);
+    pdl_set().insert(fn);
+}
+bool is_pdl_kernel(const void* fn) {
+    std::lock_guard<std::mutex> g(g_pdl_mu);
+    return pdl_set().count(fn) != 0;
+}
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 // pool.cu
@@ -325,6 +356,38 @@ extern "C" {
 int bd_abi_version(void) { return BD_ABI_VERSION; }
 const char* bd_last_error(void) { return g_last_error.c_str(); }
 uint64_t bd_launch_count(void) { return launch_count(); }
+
+int bd_trace_enable(uint32_t capacity) {
+    return guarded([&] {
+        if (g_tr_buf) {
+            cudaFree(g_tr_buf);
+            cudaFree(g_tr_cnt);
+            g_tr_buf = nullptr;
+            g_tr_cnt = nullptr;
+        }
+        g_tr_cap = capacity;
+        if (capacity) {
+            BD_CUDA(cudaMalloc(&g_tr_buf, sizeof(TraceRec) * capacity));
+            BD_CUDA(cudaMalloc(&g_tr_cnt, sizeof(unsigned)));
+            BD_CUDA(cudaMemset(g_tr_cnt, 0, sizeof(unsigned)));
+        }
+        for (TraceBinder b : trace_binders()) b(g_tr_buf, g_tr_cnt, g_tr_cap);
+        BD_CUDA(cudaDeviceSynchronize());
+    });
+}
+
+int bd_trace_read(void* out, uint32_t capacity, uint32_t* n_out) {
+    return guarded([&] {
+        require(g_tr_buf != nullptr, BD_ERR_BAD_ARGUMENT, "trace: not enabled");
+        BD_CUDA(cudaDeviceSynchronize());
+        unsigned n = 0;
+        BD_CUDA(cudaMemcpy(&n, g_tr_cnt, sizeof(n), cudaMemcpyDeviceToHost));
+        n = std::min(n, std::min(g_tr_cap, capacity));
+        if (n) BD_CUDA(cudaMemcpy(out, g_tr_buf, sizeof(TraceRec) * n, cudaMemcpyDeviceToHost));
+        BD_CUDA(cudaMemset(g_tr_cnt, 0, sizeof(unsigned)));
+        if (n_out) *n_out = n;
+    });
+}
 
 int bd_device_check(int device) {
     return guarded([&] {

@@ -320,11 +320,24 @@ __device__ __forceinline__ void bulk_load_w(void* smem_dst, const void* src, uin
 // visible) before touching anything the predecessor produced. A no-op when the
 // kernel was launched without the attribute.
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Allow the dependent (PDL-launched) grid to be scheduled now: its CTAs start their
+// predecessor-independent prologue (constant plane/weight loads) while this grid runs;
+// they still block in griddep_wait() until this grid has completed.
+#ifndef BD_LINEAR_TRIGGER
+#define BD_LINEAR_TRIGGER 0  // 1: K2 / K3 let the next glue kernel be scheduled at entry (measured: glue CTAs parked beside the linears slow them)
+#endif
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 inline bool pdl_enabled() {
     static const bool on = !(std::getenv("BD_PDL") && std::getenv("BD_PDL")[0] == '0');
     return on;
 }
+// kernels launched through launch_pdl() wait (griddep_wait) before consuming their
+// predecessors' outputs, so a captured graph may give them programmatic in-edges
+void note_pdl_kernel(const void* fn);
+bool is_pdl_kernel(const void* fn);
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args&&... args) {
@@ -338,6 +351,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    note_pdl_kernel(reinterpret_cast<const void*>(kern));
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
@@ -349,5 +363,51 @@ __device__ __forceinline__ uint32_t warp_id() {
 __device__ __forceinline__ float bf16_to_f32(uint16_t v) {
     return __uint_as_float(static_cast<uint32_t>(v) << 16);
 }
+
+// ---- optional device timeline (bd_trace_enable; tools/timeline.py) ----
+// Thread 0 of every CTA of the decode-step kernels appends one record: entry time,
+// time its griddepcontrol.wait returned, and exit time (%globaltimer, ns).
+struct TraceRec {
+    uint32_t kind, cta, smid, pad;
+    unsigned long long t_entry, t_wait, t_end;
+};
+enum : uint32_t { TR_LUT = 1, TR_GEMM = 2, TR_NORM = 3, TR_ATTN = 4, TR_SILU = 5 };
+using TraceBinder = void (*)(TraceRec*, unsigned*, unsigned);
+int trace_register(TraceBinder b);
+namespace {
+// one copy per translation unit (no -rdc): every TU registers its binder at load time
+__device__ TraceRec* g_trace_buf = nullptr;
+__device__ unsigned* g_trace_cnt = nullptr;
+__device__ unsigned g_trace_cap = 0;
+void trace_bind_tu(TraceRec* b, unsigned* c, unsigned cap) {
+    cudaMemcpyToSymbol(g_trace_buf, &b, sizeof(b));
+    cudaMemcpyToSymbol(g_trace_cnt, &c, sizeof(c));
+    cudaMemcpyToSymbol(g_trace_cap, &cap, sizeof(cap));
+}
+[[maybe_unused]] const int g_trace_reg = trace_register(&trace_bind_tu);
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ bool tracing() { return g_trace_buf != nullptr; }
+__device__ __forceinline__ void trace_rec(uint32_t kind, unsigned long long t_entry, unsigned long long t_wait) {
+    TraceRec* b = g_trace_buf;
+    if (!b) return;
+    const unsigned i = atomicAdd(g_trace_cnt, 1u);
+    if (i >= g_trace_cap) return;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    TraceRec r;
+    r.kind = kind;
+    r.cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    r.smid = smid;
+    r.pad = 0;
+    r.t_entry = t_entry;
+    r.t_wait = t_wait;
+    r.t_end = gtimer();
+    b[i] = r;
+}
+}  // namespace
 
 }  // namespace bd

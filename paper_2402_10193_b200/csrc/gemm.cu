@@ -52,6 +52,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                      const __grid_constant__ CUtensorMap map_x, float* __restrict__ partial,
                      int M, int N_valid, int bn, int kb_total, int kb_per_split, int stages) {
     extern __shared__ uint8_t smem_raw[];
+    const unsigned long long t_entry = gtimer();
+    unsigned long long t_wait = 0;
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     const GemmSmemLayout L = gemm_layout(bn, stages);
@@ -89,24 +91,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t taddr = *tmem_slot;
-    griddep_wait();  // PDL: the activations come from the previous kernel
+    if (BD_LINEAR_TRIGGER) griddep_launch_dependents();  // the next glue kernel may be scheduled
 
     if (warp == 0 && lane == 0) {
         // ---- TMA producer ----
+        // The weights do not depend on the predecessor kernel: the first ring's worth is
+        // requested before waiting for it (PDL), the activations only after.
         const uint64_t pol_w = policy_evict_first();  // weights stream once per step
+        const int npre = min(nkb, stages);
+        for (int i = 0; i < npre; ++i) {
+            mbar_arrive_expect_tx(&full[i], L.stage_bytes);
+            tma_load_2d_hint(smem + i * L.stage_bytes, &map_w, &full[i], (kb0 + i) * kBK, m0, pol_w);
+        }
+        griddep_wait();  // PDL: the activations come from the previous kernel
+        t_wait = gtimer();
         for (int i = 0; i < nkb; ++i) {
             const int s = i % stages;
             const uint32_t round = i / stages;
-            mbar_wait(&empty[s], (round & 1) ^ 1);
             uint8_t* a = smem + s * L.stage_bytes;
             uint8_t* b = a + L.a_bytes;
-            mbar_arrive_expect_tx(&full[s], L.stage_bytes);
             const int kc = (kb0 + i) * kBK;
-            tma_load_2d_hint(a, &map_w, &full[s], kc, m0, pol_w);
+            if (i >= npre) {
+                mbar_wait(&empty[s], (round & 1) ^ 1);
+                mbar_arrive_expect_tx(&full[s], L.stage_bytes);
+                tma_load_2d_hint(a, &map_w, &full[s], kc, m0, pol_w);
+            }
             tma_load_2d(b, &map_x, &full[s], kc, 0);
         }
     } else if (warp == 1 && lane == 0) {
-        // ---- MMA issuer ----
+        // ---- MMA issuer ---- (consumes only what the producer's barriers release)
         const uint32_t idesc = idesc_bf16_f32(kBM, bn);
         for (int i = 0; i < nkb; ++i) {
             const int s = i % stages;
@@ -154,6 +167,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         else if (tmem_cols_needed == 128) tmem_dealloc<128>(taddr);
         else tmem_dealloc<256>(taddr);
     }
+    if (warp == 0 && lane == 0) trace_rec(TR_GEMM, t_entry, t_wait);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {

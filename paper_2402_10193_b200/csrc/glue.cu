@@ -22,6 +22,10 @@ void note_launch();
 
 namespace {
 
+#ifndef BD_PDL_EARLY
+#define BD_PDL_EARLY 1  // glue kernels let the next (PDL) kernel start its prologue at once
+#endif
+
 constexpr int kNormChunk = 256;  // elements per block in the residual/norm kernels
 
 // k-th partial of output (b, m): base split-K partials first, then delta partials
@@ -181,7 +185,10 @@ __global__ void __launch_bounds__(kRnThreads)
                       unsigned* __restrict__ arrive, double* __restrict__ msq_part) {
     __shared__ double red_d[32];
     __shared__ double inv_s;
+    const unsigned long long t_entry = gtimer();
+    if (BD_PDL_EARLY) griddep_launch_dependents();  // next linear's prologue may start
     griddep_wait();  // PDL: the projection partials come from the previous kernel
+    const unsigned long long t_wait = gtimer();
     const int b = blockIdx.y, nc = gridDim.x;
     const int i = blockIdx.x * kRnChunk + 4 * threadIdx.x;
     const bool on = i < dim;
@@ -225,6 +232,7 @@ __global__ void __launch_bounds__(kRnThreads)
         *reinterpret_cast<uint2*>(xn + size_t(b) * ldxn + i) = pk;
     }
     if (xn_f32) *reinterpret_cast<float4*>(xn_f32 + size_t(b) * dim + i) = make_float4(y0, y1, y2, y3);
+    if (threadIdx.x == 0) trace_rec(TR_NORM, t_entry, t_wait);
 }
 
 // single-kernel variant: one 1024-thread block per request does the residual add,
@@ -495,17 +503,21 @@ __global__ void __launch_bounds__(kA2Threads)
     uint16_t* st = reinterpret_cast<uint16_t*>(vs + hd);            // [stage_rows_max][hd]: K, then V, then partials
     float* scores = reinterpret_cast<float*>(st + stage_rows_max * hd);  // max_seq
     __shared__ float red[32];
-    griddep_wait();  // PDL: q/k/v partials come from the previous kernel
+    const unsigned long long t_entry = gtimer();
+    if (BD_PDL_EARLY) griddep_launch_dependents();  // next linear's prologue may start
     const int h = blockIdx.x, b = blockIdx.y;
     const int group = a.n_heads / a.n_kv_heads;
     const int kh = h / group;
-    const int pos = pos_dev[b];
+    const int pos = pos_dev[b];  // uploaded before the step's first kernel
     const int n_ctx = pos + 1;
     const int rs = threadIdx.x >> 4, dg = threadIdx.x & 15;
     uint16_t* kc = a.kcache[b] + (static_cast<size_t>(a.layer) * a.max_seq) * a.kv_dim + kh * hd;
     uint16_t* vc = a.vcache[b] + (static_cast<size_t>(a.layer) * a.max_seq) * a.kv_dim + kh * hd;
-    // row `pos` is this step's own key/value (taken from smem below, never read from the cache)
+    // The cached rows are from earlier steps: staged before waiting for the predecessor.
+    // Row `pos` is this step's own key/value (taken from smem below, never read from the cache).
     stage_rows(st, kc, 0, min(n_ctx, stage_rows_max), a.kv_dim);
+    griddep_wait();  // PDL: q/k/v partials come from the previous kernel
+    const unsigned long long t_wait = gtimer();
 
     // q, k, v of this step (split-K + tenant delta), RoPE (same as attn_kernel)
     const float2* rope = a.rope + static_cast<size_t>(pos) * half;
@@ -614,6 +626,7 @@ __global__ void __launch_bounds__(kA2Threads)
         for (int r = 0; r < 16; ++r) t += part[r * hd + threadIdx.x];
         ctx_out[size_t(b) * ld_ctx + h * hd + threadIdx.x] = f32_to_bf16(t);
     }
+    if (threadIdx.x == 0) trace_rec(TR_ATTN, t_entry, t_wait);
 }
 
 // act = silu(gate) * up (serve.cpp:301-302)
@@ -628,7 +641,10 @@ __global__ void silu_kernel(ProjOut gu, int inter, uint16_t* __restrict__ act, i
 }
 // 4 outputs per thread (aligned shapes), same per-element arithmetic
 __global__ void silu4_kernel(ProjOut gu, int inter, uint16_t* __restrict__ act, int ld_act) {
+    const unsigned long long t_entry = gtimer();
+    if (BD_PDL_EARLY) griddep_launch_dependents();  // next linear's prologue may start
     griddep_wait();  // PDL: gate/up partials come from the previous kernel
+    const unsigned long long t_wait = gtimer();
     const int b = blockIdx.y;
     for (int i = 4 * (blockIdx.x * blockDim.x + threadIdx.x); i < inter; i += 4 * gridDim.x * blockDim.x) {
         float4 g, u;
@@ -639,6 +655,7 @@ __global__ void silu4_kernel(ProjOut gu, int inter, uint16_t* __restrict__ act, 
         pk.y = uint32_t(f(g.z, u.z)) | (uint32_t(f(g.w, u.w)) << 16);
         *reinterpret_cast<uint2*>(act + size_t(b) * ld_act + i) = pk;
     }
+    if (threadIdx.x == 0) trace_rec(TR_SILU, t_entry, t_wait);
 }
 
 // x[b] = embed[tok_b] + raw embed delta row (serve.cpp:230-236)

@@ -81,7 +81,10 @@ __global__ void __maxnreg__(kLutRegs)
                float* __restrict__ out) {
     extern __shared__ float T[];
     __shared__ float xs[32 * 33];  // x of the slice, [lane][32 columns] padded to 33
+    const unsigned long long t_entry = gtimer();
+    if (BD_LINEAR_TRIGGER) griddep_launch_dependents();  // the next glue kernel may be scheduled
     griddep_wait();  // PDL: X comes from the previous kernel; D is still read by it
+    const unsigned long long t_wait = gtimer();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int kWarps = kLutThreads / 32;
     const uint32_t lb0 = 4u * lane, lb1 = 4u * lane + 128u;  // low byte of the entry offset
@@ -91,10 +94,13 @@ __global__ void __maxnreg__(kLutRegs)
     const long long g0 = total * blockIdx.x / gridDim.x;
     const long long g1 = total * (blockIdx.x + 1) / gridDim.x;
     int cur = -1;
-    for (long long g = g0; g < g1;) {
+    // rows [ga, gb) of the flattened (unit, row) space; CTA-uniform (tables are rebuilt
+    // with block barriers when the range enters a new unit)
+    auto run_range = [&](long long ga, long long gb) {
+    for (long long g = ga; g < gb;) {
         const int u = static_cast<int>(g / p.M);
         const int ra = static_cast<int>(g % p.M);
-        const int rb = static_cast<int>(std::min<long long>(p.M, ra + (g1 - g)));
+        const int rb = static_cast<int>(std::min<long long>(p.M, ra + (gb - g)));
         const int job_i = u / p.slices, slice = u % p.slices;
         const LutJob& job = p.jobs[job_i];
         const int c0 = slice * kSliceCols;
@@ -171,6 +177,12 @@ __global__ void __maxnreg__(kLutRegs)
         }
         g += rb - ra;
     }
+    };
+    run_range(g0, g1);
+    if (tracing()) {
+        __syncthreads();
+        if (threadIdx.x == 0) trace_rec(TR_LUT, t_entry, t_wait);
+    }
 }
 
 }  // namespace
@@ -213,9 +225,13 @@ void lut_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t st
         // helps when plane rows are 128-B aligned (qkv/o/gu: -0.34 ms/step) and hurts
         // the down projection (1376-B rows, every warp load spans two lines: +0.35 ms),
         // where the default carveout keeps the two kernels on mostly disjoint SMs.
-        if (kWPR % 32 == 0 && kWPR > 0)
+        static const bool carve_all = std::getenv("BD_LUT_CARVE_ALL") && std::getenv("BD_LUT_CARVE_ALL")[0] == '1';
+        static const int carve_un = std::getenv("BD_LUT_CARVE_UN") ? std::atoi(std::getenv("BD_LUT_CARVE_UN")) : -1;
+        if ((kWPR % 32 == 0 && kWPR > 0) || carve_all)
             BD_CUDA(cudaFuncSetAttribute(lut_kernel<kWPR>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          int(cudaSharedmemCarveoutMaxShared)));
+        else if (carve_un >= 0)
+            BD_CUDA(cudaFuncSetAttribute(lut_kernel<kWPR>, cudaFuncAttributePreferredSharedMemoryCarveout, carve_un));
         attr = true;
     }
     BD_CUDA(launch_pdl(lut_kernel<kWPR>, dim3(p.grid), dim3(kLutThreads), kTableBytes, stream, p,

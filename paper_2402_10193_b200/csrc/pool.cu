@@ -193,6 +193,7 @@ struct PoolImpl {
     cudaStream_t stream2 = nullptr;  // side stream: K2 beside K3
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool concurrent_k23 = true;      // BD_SERIAL=1 disables
+    bool pdl_edges = true;           // BD_PDL_EDGES=0 keeps captured cross-stream edges full
     bool use_graphs = true;
     // timing experiments only (results are wrong): BD_SKIP bitmask drops launches of
     // 1 norm, 2 attention, 4 silu, 8 K3 delta, 16 K2 gemm
@@ -265,6 +266,7 @@ struct PoolImpl {
         BD_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
         BD_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
         if (const char* e = std::getenv("BD_SERIAL")) concurrent_k23 = (e[0] == '0');
+        if (const char* e = std::getenv("BD_PDL_EDGES")) pdl_edges = (e[0] != '0');
         BD_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         BD_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
         if (const char* e = std::getenv("BD_NO_GRAPH")) use_graphs = (e[0] == '0');
@@ -1097,7 +1099,9 @@ struct PoolImpl {
             static const int b1_cap = 190;
             for (int gi = 0; gi < 4; ++gi)
                 if (p->lut[0][gi].ok) {
-                    const int cap = b1_supported(p->lut[0][gi].prm) ? b1_cap * 1024 : 88 * 1024;
+                    int cap = b1_supported(p->lut[0][gi].prm) ? b1_cap * 1024 : 88 * 1024;
+                    static const char* cap3 = std::getenv("BD_K2_CAP_DOWN");
+                    if (gi == 3 && cap3) cap = std::atoi(cap3) * 1024;
                     *gs[gi] = plan_base_gemm(gs[gi]->M, gs[gi]->K, B, cap);
                     require(uint64_t(gs[gi]->splits) * B * gs[gi]->M <= P_elems, BD_ERR_CUDA,
                             "split-K workspace too small");
@@ -1334,11 +1338,43 @@ struct PoolImpl {
             }
             BD_CUDA(cudaStreamEndCapture(stream, &graph));
             kcount = launch_count() - c0;
+            if (pdl_edges) promote_programmatic_edges(graph);
             BD_CUDA(cudaGraphInstantiate(&g, graph, 0));
             BD_CUDA(cudaGraphDestroy(graph));
         }
         BD_CUDA(cudaGraphLaunch(g, stream));
         stats.kernels_last_step = kcount;
+    }
+
+    // Stream capture turns the fork/join of K2 (side stream) into full dependencies;
+    // every kernel-to-kernel edge whose consumer waits in griddep_wait() before touching
+    // its inputs becomes programmatic, so K2 (and the glue after a join) is scheduled
+    // while its predecessor drains and streams its constant weights meanwhile.
+    static void promote_programmatic_edges(cudaGraph_t graph) {
+        size_t n = 0;
+        BD_CUDA(cudaGraphGetEdges_v2(graph, nullptr, nullptr, nullptr, &n));
+        std::vector<cudaGraphNode_t> from(n), to(n);
+        std::vector<cudaGraphEdgeData> ed(n);
+        BD_CUDA(cudaGraphGetEdges_v2(graph, from.data(), to.data(), ed.data(), &n));
+        auto kernel_fn = [](cudaGraphNode_t nd) -> const void* {
+            cudaGraphNodeType t;
+            BD_CUDA(cudaGraphNodeGetType(nd, &t));
+            if (t != cudaGraphNodeTypeKernel) return nullptr;
+            cudaKernelNodeParams kp{};
+            BD_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
+            return kp.func;
+        };
+        for (size_t i = 0; i < n; ++i) {
+            if (ed[i].type != cudaGraphDependencyTypeDefault) continue;
+            if (!kernel_fn(from[i])) continue;
+            const void* f = kernel_fn(to[i]);
+            if (!f || !is_pdl_kernel(f)) continue;
+            BD_CUDA(cudaGraphRemoveDependencies_v2(graph, &from[i], &to[i], &ed[i], 1));
+            cudaGraphEdgeData e{};
+            e.from_port = cudaGraphKernelNodePortProgrammatic;
+            e.type = cudaGraphDependencyTypeProgrammatic;
+            BD_CUDA(cudaGraphAddDependencies_v2(graph, &from[i], &to[i], &e, 1));
+        }
     }
 
     void validate(const bd_request* reqs, uint64_t n) {
