@@ -162,6 +162,25 @@ void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stre
 bool b1_supported(const LutParams& p);
 void b1_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream);
 
+// ---- K3t: tenant deltas alone on the FP4 tensor cores, beside K2 (mxd.cu) ----
+// Same work and output as the LUT plan (D[slice][batch][M], alpha applied); one sign
+// plane per (job, segment), segment rows % 128 == 0, activations as FP4 pieces (xp_prep).
+struct MxdJob {
+    int req;
+    float alpha[kLutMaxSegs];
+};
+struct MxdParams {
+    const CUtensorMap* maps;  // device table [n_jobs * n_segs] (tmap_bits4)
+    const uint8_t* xpk;       // [batch][n_chunks][kXpBlock]
+    long long total_stages;
+    int n_jobs, n_segs, M, m_tiles, cols, batch, slices, n_chunks, grid, smem;
+    int seg_row0[kLutMaxSegs + 1];
+    MxdJob jobs[kLutMaxJobs];
+};
+// Fills the geometry from n_jobs/jobs and the segment rows; false if unsupported (BD_MXD=0 disables).
+bool plan_mxd(MxdParams& p, const int* seg_rows, int n_segs, int cols, int batch);
+void mxd_launch(const MxdParams& p, float* out, cudaStream_t stream);
+
 // Y[b][m] = sum_s P[s][b][m] (+ D[b][m])
 void combine_launch(const float* P, int splits, const float* D, int batch, int M, float* Y,
                     cudaStream_t stream, int dsplits = 1);

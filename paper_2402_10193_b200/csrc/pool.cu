@@ -131,6 +131,8 @@ struct Plan {
     struct Lut {
         bool ok = false;
         LutParams prm;
+        bool mxd = false;  // K3t (FP4 tensor cores) instead of the byte LUT for this group
+        MxdParams mx;
     };
     std::vector<std::array<Lut, 4>> lut;
     // K23 (base + FP4 tensor-core deltas in one kernel) per layer & group
@@ -754,6 +756,76 @@ struct PoolImpl {
             if (!ok)
                 for (uint64_t l = 0; l < nL; ++l) p.lut[l][gi].ok = false;
         }
+        plan_mxd_groups(p);
+    }
+
+    // K3t (mxd.cu) for the LUT-planned groups: one plane per (request, segment), 128-row
+    // aligned segments; the plane tensor maps live in one device table per plan
+    void plan_mxd_groups(Plan& p) {
+        const int B = p.B;
+        const uint64_t nL = a.n_layers;
+        std::vector<CUtensorMap> maps;
+        std::vector<std::pair<uint64_t, int>> users;  // (layer, group) -> first map index
+        std::vector<size_t> first;
+        for (int gi = 0; gi < 4; ++gi) {
+            if (nL == 0 || !p.lut[0][gi].ok) continue;
+            {   // shape checks before any tensor map is encoded (TMA needs 16-byte row strides)
+                MxdParams probe{};
+                probe.n_jobs = 1;
+                const LutParams& lp = p.lut[0][gi].prm;
+                int seg_rows[kLutMaxSegs];
+                for (int sg = 0; sg < lp.n_segs; ++sg) seg_rows[sg] = lp.seg_row0[sg + 1] - lp.seg_row0[sg];
+                if (!plan_mxd(probe, seg_rows, lp.n_segs, lp.cols, B)) continue;
+            }
+            bool ok = true;
+            std::vector<size_t> idx(nL);
+            std::vector<MxdParams> prms(nL);
+            for (uint64_t l = 0; l < nL && ok; ++l) {
+                const LutParams& lp = p.lut[l][gi].prm;
+                MxdParams& m = prms[l];
+                m = MxdParams{};
+                m.n_jobs = lp.n_jobs;
+                int seg_rows[kLutMaxSegs];
+                for (int sg = 0; sg < lp.n_segs; ++sg) seg_rows[sg] = lp.seg_row0[sg + 1] - lp.seg_row0[sg];
+                idx[l] = maps.size();
+                for (int j = 0; j < lp.n_jobs && ok; ++j) {
+                    m.jobs[j].req = lp.jobs[j].req;
+                    for (int sg = 0; sg < lp.n_segs; ++sg) {
+                        if (lp.jobs[j].n_planes[sg] != 1 ||
+                            reinterpret_cast<uintptr_t>(lp.jobs[j].bits[sg][0]) % 16) {
+                            ok = false;
+                            break;
+                        }
+                        m.jobs[j].alpha[sg] = lp.jobs[j].alpha[sg][0];
+                        maps.push_back(tmap_bits4(lp.jobs[j].bits[sg][0], uint64_t(seg_rows[sg]), uint64_t(lp.cols)));
+                    }
+                }
+                ok = ok && plan_mxd(m, seg_rows, lp.n_segs, lp.cols, B);
+            }
+            if (!ok) {
+                maps.resize(idx.empty() ? maps.size() : idx[0]);
+                continue;
+            }
+            for (uint64_t l = 0; l < nL; ++l) {
+                p.lut[l][gi].mx = prms[l];
+                p.lut[l][gi].mxd = true;
+                first.push_back(idx[l]);
+                users.push_back({l, gi});
+            }
+        }
+        if (users.empty()) return;
+        CUtensorMap* d = dmalloc<CUtensorMap>(maps.size(), &p.allocs);
+        BD_CUDA(cudaMemcpy(d, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+        const int max_chunks = xp_chunks(int(std::max(a.dim, a.intermediate)));
+        if (!p.xpk) {
+            p.xpk = dmalloc<uint8_t>(size_t(B) * max_chunks * kXpBlock, &p.allocs);
+            BD_CUDA(cudaMemset(p.xpk, 0, size_t(B) * max_chunks * kXpBlock));
+        }
+        for (size_t u = 0; u < users.size(); ++u) {
+            MxdParams& m = p.lut[users[u].first][users[u].second].mx;
+            m.maps = d + first[u];
+            m.xpk = p.xpk;
+        }
     }
 
     // K23 (mt4.cu): base GEMM + every tenant plane as FP4 MMAs in one persistent
@@ -1192,9 +1264,16 @@ struct PoolImpl {
                 // fork the GEMM onto the side stream, join before the consumer.
                 // Profiled as one unit (kind FUSED_*: all of K2+K3 for the group).
                 prof(BD_PROF_FUSED_QKV + group, s, [&] {
+                    // K3t: the FP4 pieces first, so the delta kernel (PDL) claims its SM
+                    // slots before K2 (side stream) could take two CTAs per SM
+                    const bool mxd = p.lut[l][group].mxd && !(skip & 8);
+                    if (mxd) xp_prep_launch(X, ldx, cols, B, p.xpk, s);
                     BD_CUDA(cudaEventRecord(ev_fork, s));
                     BD_CUDA(cudaStreamWaitEvent(stream2, ev_fork, 0));
-                    if (!(skip & 8)) lut_launch(p.lut[l][group].prm, X, D, s);
+                    if (mxd)
+                        mxd_launch(p.lut[l][group].mx, D, s);
+                    else if (!(skip & 8))
+                        lut_launch(p.lut[l][group].prm, X, D, s);
                     if (!(skip & 16)) base_gemm_launch(g, mw, mx, P, stream2);
                     BD_CUDA(cudaEventRecord(ev_join, stream2));
                     BD_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
