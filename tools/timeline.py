@@ -128,6 +128,21 @@ def main():
                      " ".join(f"{c}:{ends[nk == c].mean():.2f}(n={int((nk == c).sum())})" for c in sorted(set(nk.tolist()))) +
                      f"; by smid>=74: {ends[die == 0].mean():.2f}/{ends[die == 1].mean():.2f}; "
                      f"corr(end, cta)={np.corrcoef(ends, r['cta'].astype(np.float64))[0, 1]:.2f}")
+    # per-SM lateness of the LUT launches: is the same SM late in every launch?
+    lut = [r for k, r in L if k == 1]
+    if len(lut) >= 8:
+        M = np.full((len(lut), 160), np.nan)
+        for i, r in enumerate(lut):
+            e = (r["t_end"].astype(np.float64) - np.median(r["t_end"].astype(np.float64))) / 1e3
+            M[i, r["smid"].astype(np.int64)] = e
+        half = len(lut) // 2
+        a_ = np.nanmean(M[:half], axis=0)
+        b_ = np.nanmean(M[half:], axis=0)
+        ok = ~np.isnan(a_) & ~np.isnan(b_)
+        lines.append(f"# LUT per-SM lateness: corr(first half of launches, second half) = "
+                     f"{np.corrcoef(a_[ok], b_[ok])[0, 1]:.2f}; per-SM mean lateness std {np.nanstd(np.nanmean(M, axis=0)):.2f} us, "
+                     f"per-launch std {np.nanmean(np.nanstd(M, axis=1)):.2f} us")
+        np.save(os.path.join(os.path.dirname(args.out), "lut_sm_lateness.npy"), M)
     txt = "\n".join(lines)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     open(args.out, "w").write(txt + "\n")
