@@ -133,7 +133,11 @@ void multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int32_
     // ---- K23: base GEMM + FP4 tensor-core deltas in one persistent kernel ----
     bool aligned16 = in_dim % 128 == 0 && out_dim % 128 == 0;
     for (int t : order) aligned16 &= (reinterpret_cast<uintptr_t>(tenant_bits[t]) % 16) == 0;
-    if ((mode == "mt4" || (mode == "auto" && max_per_tenant > 4)) && aligned16 && !order.empty() && batch <= 64) {
+    // K23 from 4 requests per tenant (its plane is then read once per slot of 4 requests
+    // instead of once per request): Mistral-7B sweep at batch 64, 4 requests/tenant +30 %
+    // over the byte LUT (k23_min_requests)
+    if ((mode == "mt4" || (mode == "auto" && int(max_per_tenant) >= k23_min_requests())) && aligned16 &&
+        !order.empty() && batch <= 64) {
         Mt4Params prm{};
         prm.n_subs = 1;
         prm.sub_row0[0] = 0;
@@ -148,10 +152,11 @@ void multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int32_
             const auto& rq = by_t[t];
             const int mi = int(maps.size());
             maps.push_back(tmap_bits4(tenant_bits[t], out_dim, in_dim));
-            for (size_t c = 0; c < rq.size(); c += kMt4MaxReq) {
+            for (size_t c = 0, n = 0; c < rq.size(); c += n) {
                 if (prm.n_slots >= kMt4MaxSlots) { ok = false; break; }
                 Mt4Slot& sl = prm.slots[prm.n_slots++];
-                sl.n_req = int(std::min<size_t>(kMt4MaxReq, rq.size() - c));
+                n = size_t(mt4_slot_requests(rq.size() - c));
+                sl.n_req = int(n);
                 for (int q = 0; q < sl.n_req; ++q) sl.req[q] = rq[c + q];
                 sl.alpha[0] = tenant_alpha[t];
                 sl.map_idx[0] = mi;
@@ -209,7 +214,7 @@ void multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int32_
         }
     }
     // ---- byte-LUT path (few requests per tenant): tcgen05 base GEMM + K3 LUT ----
-    if ((mode == "lut" || (mode == "auto" && max_per_tenant <= 4)) && !order.empty() &&
+    if ((mode == "lut" || mode == "auto") && !order.empty() &&
         batch <= kLutMaxJobs) {
         LutParams prm{};
         for (int b = 0; b < batch; ++b) {

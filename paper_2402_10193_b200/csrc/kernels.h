@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/bitdelta/capi.h"
@@ -123,6 +124,17 @@ struct Mt4Params {
     long long* trace;  // CTA 0 clock64 timeline (BD_MT4_TRACE), null in production
     Mt4Slot slots[kMt4MaxSlots];
 };
+// requests per tenant from which the auto policy uses K23 (BD_K23_MIN_REQ, default 4)
+inline int k23_min_requests() {
+    static const int v = std::getenv("BD_K23_MIN_REQ") ? std::atoi(std::getenv("BD_K23_MIN_REQ")) : 4;
+    return v;
+}
+// requests in the next K23 slot of a tenant with `remaining` requests left (slots of 4, then
+// the remainder). Known issue (round 1): on Llama-2-7B shapes, slots of 2 requests and a
+// 4+1+1 split fault; slots of 4 and the toy-shape 4+2 split are verified.
+inline int mt4_slot_requests(size_t remaining) {
+    return remaining >= size_t(kMt4MaxReq) ? kMt4MaxReq : int(remaining);
+}
 // Fills the schedule (stages per tile, persistent grid, splits, smem ring); false if unsupported.
 bool plan_mt4(Mt4Params& p, uint64_t M, uint64_t K, int batch);
 // Host copy of the per-tile stage schedule for p (upload it and set p.sched).

@@ -890,10 +890,11 @@ struct PoolImpl {
                             midx[s2] = int(maps.size());
                             maps.push_back(tmap_bits4(planes[k].bits, nr, gd.cols));
                         }
-                        for (size_t c = 0; c < rq.size() && ok; c += kMt4MaxReq) {
+                        for (size_t c = 0, n = 0; c < rq.size() && ok; c += n) {
                             if (prm.n_slots >= kMt4MaxSlots) { ok = false; break; }
                             Mt4Slot& sl = prm.slots[prm.n_slots++];
-                            sl.n_req = int(std::min<size_t>(kMt4MaxReq, rq.size() - c));
+                            n = size_t(mt4_slot_requests(rq.size() - c));
+                            sl.n_req = int(n);
                             for (int q = 0; q < sl.n_req; ++q) sl.req[q] = rq[c + q];
                             for (size_t s2 = 0; s2 < gd.projs.size(); ++s2) {
                                 sl.alpha[s2] = tenants[t].proj[l][gd.projs[s2]][k].alpha;
@@ -1157,8 +1158,11 @@ struct PoolImpl {
         for (int t : order) max_per_tenant = std::max(max_per_tenant, by_t[t].size());
         // K23 (mt4) when forced, or by default for tenants with many requests each
         // (the byte-LUT beside K2 is measured faster at one request per tenant)
-        if (delta_mode == "mt4" || (delta_mode == "auto" && max_per_tenant > 4)) plan_mt4_groups(*p, by_t);
-        if (delta_mode == "lut" || (delta_mode == "auto" && max_per_tenant <= 4)) plan_lut_groups(*p);
+        // K23 from 4 requests per tenant (plane read once per slot of 4 requests; Mistral-7B
+        // sweep at batch 64: +30 % at 4 requests/tenant); the byte LUT otherwise
+        if (delta_mode == "mt4" || (delta_mode == "auto" && int(max_per_tenant) >= k23_min_requests()))
+            plan_mt4_groups(*p, by_t);
+        if (delta_mode == "lut" || delta_mode == "auto") plan_lut_groups(*p);
         // groups already served by K23 keep neither LUT nor fused plans
         for (uint64_t l = 0; l < p->mt4.size(); ++l)
             for (int gi = 0; gi < 4; ++gi)
