@@ -280,22 +280,22 @@ def test_head_dim_128_long_context_matches_port(cuda, port):
     pool.close()
 
 
-def _k23_pool_run(port, B_per_t, steps):
-    """Two tenants x B_per_t requests each on a 128-multiple shape (K23-eligible),
+def _k23_pool_run(port, B_per_t, steps, n_tenants=2, dim=256, inter=512, n_layers=2):
+    """n_tenants tenants x B_per_t requests each on a 128-multiple shape (K23-eligible),
     several decode steps against the port on the same bf16 backbone."""
-    arch = dict(vocab=64, dim=256, n_layers=2, n_heads=2, intermediate=512, max_seq=16,
-                rope_theta=10000.0, kv_dim=256)
+    arch = dict(vocab=64, dim=dim, n_layers=n_layers, n_heads=dim // 128, intermediate=inter, max_seq=16,
+                rope_theta=10000.0, kv_dim=dim)
     rng = np.random.default_rng(11)
     tens = {}
     for name, r, c in tensor_shapes(arch):
         w = rng.standard_normal((r, c)).astype(np.float32) * (1.0 if r == 1 else 0.05)
         tens[name] = bf16_round(w + (1.0 if r == 1 else 0.0))
     pool = ServingPool(arch, tens)
-    ents = [_random_entries(arch, rng) for _ in range(2)]
+    ents = [_random_entries(arch, rng) for _ in range(n_tenants)]
     for t, e in enumerate(ents):
         pool.register_delta_entries(f"t{t}", e)
-    B = 2 * B_per_t
-    rids = [pool.open_request(f"t{b % 2}") for b in range(B)]
+    B = n_tenants * B_per_t
+    rids = [pool.open_request(f"t{b % n_tenants}") for b in range(B)]
     names = [n for n, _, _ in tensor_shapes(arch)]
     port_ents = [[{k: v for k, v in e.items()} for e in es] for es in ents]
     for es in port_ents:
@@ -303,13 +303,13 @@ def _k23_pool_run(port, B_per_t, steps):
             if e["kind"] == "raw":
                 e["raw"] = e["raw"].reshape(-1)
     flat = np.concatenate([tens[n].reshape(-1) for n in names])
-    kc = [np.zeros((2, arch["max_seq"], arch["kv_dim"]), np.float32) for _ in range(B)]
+    kc = [np.zeros((arch["n_layers"], arch["max_seq"], arch["kv_dim"]), np.float32) for _ in range(B)]
     vc = [np.zeros_like(k) for k in kc]
     errs = []
     for pos in range(steps):
         toks = [int(t) for t in rng.integers(0, arch["vocab"], B)]
         got = pool.decode_step([(r, toks[i], pos) for i, r in enumerate(rids)])
-        want = port.decode(arch, flat, port_ents, [b % 2 for b in range(B)], toks, [pos] * B, kc, vc)
+        want = port.decode(arch, flat, port_ents, [b % n_tenants for b in range(B)], toks, [pos] * B, kc, vc)
         errs.append(max(rel_l2(got[i], want[i]) for i in range(B)))
     pool.close()
     return max(errs)
@@ -356,4 +356,25 @@ print('ok')
 """
     env = dict(os.environ, BD_MXD="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_k23_pool_two_request_slots_short_plane_ring(cuda, port):
+    """K23 with 2-request slots on one Llama-2-7B-shaped layer (8 tenants x 2 requests): the
+    plane-stage ring is then as short as the producer count, the case whose mbarrier phases
+    aliased (launch failure) before the per-slot fill guard (mt4.cu); logits against the port."""
+    import subprocess
+    import sys
+
+    code = f"""
+import sys; sys.path.insert(0, {repr(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))})
+sys.path.insert(0, {repr(os.path.dirname(os.path.abspath(__file__)))})
+import oracle
+from test_gpu_pool import _k23_pool_run
+err = _k23_pool_run(oracle.port(), 2, 1, n_tenants=8, dim=4096, inter=11008, n_layers=1)
+assert err <= 1e-2, err
+print('ok')
+"""
+    env = dict(os.environ, BD_DELTA="mt4")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
