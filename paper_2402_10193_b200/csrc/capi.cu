@@ -136,7 +136,7 @@ void multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int32_
     // K23 from 4 requests per tenant (its plane is then read once per slot of 4 requests
     // instead of once per request): Mistral-7B sweep at batch 64, 4 requests/tenant +30 %
     // over the byte LUT (k23_min_requests)
-    if ((mode == "mt4" || (mode == "auto" && int(max_per_tenant) >= k23_min_requests())) && aligned16 &&
+    if ((mode == "mt4" || (mode == "auto" && int(max_per_tenant) >= k23_min_requests(batch))) && aligned16 &&
         !order.empty() && batch <= 64) {
         Mt4Params prm{};
         prm.n_subs = 1;

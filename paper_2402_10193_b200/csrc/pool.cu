@@ -1160,7 +1160,7 @@ struct PoolImpl {
         // (the byte-LUT beside K2 is measured faster at one request per tenant)
         // K23 from 4 requests per tenant (plane read once per slot of 4 requests; Mistral-7B
         // sweep at batch 64: +30 % at 4 requests/tenant); the byte LUT otherwise
-        if (delta_mode == "mt4" || (delta_mode == "auto" && int(max_per_tenant) >= k23_min_requests()))
+        if (delta_mode == "mt4" || (delta_mode == "auto" && int(max_per_tenant) >= k23_min_requests(B)))
             plan_mt4_groups(*p, by_t);
         if (delta_mode == "lut" || delta_mode == "auto") plan_lut_groups(*p);
         // groups already served by K23 keep neither LUT nor fused plans
