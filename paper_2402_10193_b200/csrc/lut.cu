@@ -185,6 +185,177 @@ __global__ void __maxnreg__(kLutRegs)
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// v2 (cols % 128 == 0, 16-byte aligned planes — every BASELINE shape): fewer MIO operations
+// per 32-bit row word than v1's 6 (1 LDG.32 + 4 LDS + 1 SHFL):
+//   * lane l = (chunk c = l & 7, row group g = l >> 3) loads 16 bytes (128 columns) of a row
+//     with one LDG.128 — a warp instruction covers 4 whole 128-byte row slices;
+//   * the 4 rows of a lane are reduced over the 8 chunk lanes with a 3-level transposing
+//     butterfly: 4 SHFL per 16 words (v1: 16);
+//   * lookups stay conflict-free although 4 lanes (one per row group) read each table at
+//     once: row group g reads byte (b + g) & 3 of a word in lookup slot b, and table
+//     (c, w, b') lives in bank 4c + b' — a runtime PRMT selector does the rotation for free.
+// Per word: 4 PRMT + 4 LDS + 4 FADD, 1/4 LDG, 1/4 SHFL.
+// Table entry (chunk c, word w, byte b', value e) at byte
+//   65536 (w >> 1) + 256 e + 128 (w & 1) + 4 (4c + b')   (128 KB, same footprint as v1).
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+
+__device__ __forceinline__ void build_tables_v2(float* T, const float* xs) {
+    // thread t -> bank t & 31 (c = bank >> 2, b' = bank & 3), word w = (t >> 5) & 3,
+    // quarter (t >> 7) of the 256 entries; a warp stores one 128-byte row per entry.
+    const int bank = threadIdx.x & 31, w = (threadIdx.x >> 5) & 3, quarter = threadIdx.x >> 7;
+    const int col = 128 * (bank >> 2) + 32 * w + 8 * (bank & 3);
+    float xv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) xv[i] = xs[col + i + ((col + i) >> 7)];
+    float lo[16], hi[4];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        float s = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s += (e >> i & 1) ? xv[i] : -xv[i];
+        lo[e] = s;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int eh = quarter * 4 + e;
+        float s = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s += (eh >> i & 1) ? xv[4 + i] : -xv[4 + i];
+        hi[e] = s;
+    }
+    float* Tw = T + (w >> 1) * 16384 + (w & 1) * 32 + bank;  // float index
+#pragma unroll
+    for (int eh = 0; eh < 4; ++eh)
+#pragma unroll
+        for (int el = 0; el < 16; ++el) Tw[((quarter * 4 + eh) * 16 + el) * 64] = hi[eh] + lo[el];
+}
+
+template <int kWPR>  // words per plane row (cols/32); 0 = runtime value
+__global__ void __maxnreg__(kLutRegs)
+    lut2_kernel(const __grid_constant__ LutParams p, const uint16_t* __restrict__ X,
+                float* __restrict__ out) {
+    extern __shared__ float T[];
+    __shared__ float xs[kSliceCols + kSliceCols / 128];  // x of the slice, padded every 128
+    const unsigned long long t_entry = gtimer();
+    griddep_wait();  // PDL: X comes from the previous kernel; D is still read by it
+    const unsigned long long t_wait = gtimer();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int chunk = lane & 7, grp = lane >> 3;
+    constexpr int kWarps = kLutThreads / 32;
+    constexpr int kRows = 16;  // rows per warp batch (4 per lane)
+    // per lookup slot b: PRMT selector (result byte 0 = L byte b = low byte 4*bank,
+    // byte 1 = word byte (b + grp) & 3, bytes 2-3 = sign of L byte 0 = 0)
+    uint32_t L = 0, sel[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const uint32_t bp = (b + grp) & 3;
+        L |= (16u * chunk + 4u * bp) << (8 * b);
+        sel[b] = 0xCC00u | (bp << 4) | (4u + b);
+    }
+    const char* Tc = reinterpret_cast<const char*>(T);
+    const int wpr = kWPR ? kWPR : p.cols / 32;
+    const long long total = static_cast<long long>(p.n_jobs) * p.slices * p.M;
+    const long long g0 = total * blockIdx.x / gridDim.x;
+    const long long g1 = total * (blockIdx.x + 1) / gridDim.x;
+    int cur = -1;
+    for (long long g = g0; g < g1;) {
+        const int u = static_cast<int>(g / p.M);
+        const int ra = static_cast<int>(g % p.M);
+        const int rb = static_cast<int>(std::min<long long>(p.M, ra + (g1 - g)));
+        const int job_i = u / p.slices, slice = u % p.slices;
+        const LutJob& job = p.jobs[job_i];
+        const int c0 = slice * kSliceCols;
+        if (u != cur) {
+            __syncthreads();  // previous unit's lookups done
+            const uint16_t* xr = X + static_cast<size_t>(job.req) * p.ldx;
+            for (int i = threadIdx.x; i < kSliceCols; i += kLutThreads)
+                xs[i + (i >> 7)] = (c0 + i < p.cols) ? bf16_to_f32(xr[c0 + i]) : 0.0f;
+            __syncthreads();
+            build_tables_v2(T, xs);
+            __syncthreads();
+            cur = u;
+        }
+        const bool lane_on = c0 + 128 * chunk < p.cols;
+        float* out_u = out + (static_cast<size_t>(slice) * p.batch + job.req) * p.M;
+        for (int s = 0; s < p.n_segs; ++s) {
+            const int s0 = p.seg_row0[s], s1 = p.seg_row0[s + 1];
+            const int la = std::max(ra, s0) - s0, lb = std::min(rb, s1) - s0;
+            if (la >= lb) continue;
+            const int n_planes = job.n_planes[s];
+            for (int pl = 0; pl < n_planes; ++pl) {
+                const uint4* plane = reinterpret_cast<const uint4*>(job.bits[s][pl]) + slice * 8 + chunk;
+                const float a = job.alpha[s][pl];
+                // lane rows: r0 + 4 grp + i, i < 4 (each LDG.128 instruction: 4 rows x 128 B)
+                auto load = [&](int r0, uint4 (&w)[4]) {
+                    const int rl = r0 + 4 * grp;
+                    const uint4* rowp = plane + static_cast<size_t>(rl) * (wpr / 4);
+                    if (lane_on && r0 + kRows <= lb) {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) w[i] = __ldcs(rowp + i * (wpr / 4));
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            w[i] = (lane_on && rl + i < lb) ? __ldcs(rowp + i * (wpr / 4)) : make_uint4(0, 0, 0, 0);
+                    }
+                };
+                uint4 wn[4];
+                int r0 = la + warp * kRows;
+                if (r0 < lb) load(r0, wn);
+                for (; r0 < lb; r0 += kWarps * kRows) {
+                    uint4 wc[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) wc[i] = wn[i];
+                    if (r0 + kWarps * kRows < lb) load(r0 + kWarps * kRows, wn);
+                    float acc[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t v[4] = {wc[i].x, wc[i].y, wc[i].z, wc[i].w};
+                        float sw[4];
+#pragma unroll
+                        for (int w = 0; w < 4; ++w) {
+                            const char* Tw = Tc + 65536 * (w >> 1) + 128 * (w & 1);
+                            const float t0 = *reinterpret_cast<const float*>(Tw + prmt(v[w], L, sel[0]));
+                            const float t1 = *reinterpret_cast<const float*>(Tw + prmt(v[w], L, sel[1]));
+                            const float t2 = *reinterpret_cast<const float*>(Tw + prmt(v[w], L, sel[2]));
+                            const float t3 = *reinterpret_cast<const float*>(Tw + prmt(v[w], L, sel[3]));
+                            sw[w] = (t0 + t1) + (t2 + t3);
+                        }
+                        acc[i] = a * ((sw[0] + sw[1]) + (sw[2] + sw[3]));
+                    }
+                    // transposing butterfly over the chunk bits (lane bits 2, 1), then a pair sum:
+                    // lane ends with row 2 * bit2 + bit1 of its group
+#pragma unroll
+                    for (int o = 4, n = 2; o >= 2; o >>= 1, n >>= 1) {
+                        const bool upper = (lane & o) != 0;
+#pragma unroll
+                        for (int j = 0; j < n; ++j) {
+                            const float send = upper ? acc[j] : acc[j + n];
+                            const float keep = upper ? acc[j + n] : acc[j];
+                            acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                        }
+                    }
+                    const float tot = acc[0] + __shfl_xor_sync(0xffffffffu, acc[0], 1);
+                    const int r = r0 + 4 * grp + 2 * ((lane >> 2) & 1) + ((lane >> 1) & 1);
+                    if ((lane & 1) == 0 && r < lb) {
+                        if (pl == 0) out_u[s0 + r] = tot;
+                        else out_u[s0 + r] += tot;  // same thread wrote it for plane 0
+                    }
+                }
+            }
+        }
+        g += rb - ra;
+    }
+    if (tracing()) {
+        __syncthreads();
+        if (threadIdx.x == 0) trace_rec(TR_LUT, t_entry, t_wait);
+    }
+}
+
 }  // namespace
 
 size_t lut_smem_bytes() { return kTableBytes; }
@@ -238,9 +409,50 @@ void lut_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t st
                        static_cast<const uint16_t*>(X), out));
 }
 
+template <int kWPR>
+void lut2_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t stream) {
+    static bool attr = false;
+    if (!attr) {
+        BD_CUDA(cudaFuncSetAttribute(lut2_kernel<kWPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(kTableBytes)));
+        // max carveout (K2 co-resident on every SM) where plane rows are 128-B aligned; the
+        // down projection (1376-B rows) measured faster on the default carveout (as v1)
+        static const int carve = std::getenv("BD_LUT2_CARVE") ? std::atoi(std::getenv("BD_LUT2_CARVE")) : -2;
+        if (carve >= 0 || (carve == -2 && kWPR % 32 == 0 && kWPR > 0))
+            BD_CUDA(cudaFuncSetAttribute(lut2_kernel<kWPR>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         carve >= 0 ? carve : int(cudaSharedmemCarveoutMaxShared)));
+        attr = true;
+    }
+    BD_CUDA(launch_pdl(lut2_kernel<kWPR>, dim3(p.grid), dim3(kLutThreads), kTableBytes, stream, p,
+                       static_cast<const uint16_t*>(X), out));
+}
+
+static bool lut2_ok(const LutParams& p) {
+    static const bool v1 = std::getenv("BD_LUT_V1") && std::getenv("BD_LUT_V1")[0] == '1';
+    if (v1 || p.cols % 128 != 0) return false;
+    for (int j = 0; j < p.n_jobs; ++j)
+        for (int s = 0; s < p.n_segs; ++s)
+            for (int k = 0; k < p.jobs[j].n_planes[s]; ++k)
+                if (reinterpret_cast<uintptr_t>(p.jobs[j].bits[s][k]) % 16) return false;
+    return true;
+}
+
 void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream) {
     if (b1_supported(p)) {
         b1_launch(p, X, out, stream);
+        return;
+    }
+    if (lut2_ok(p)) {
+        switch (p.cols) {
+            case 4096: lut2_launch_t<128>(p, X, out, stream); break;
+            case 8192: lut2_launch_t<256>(p, X, out, stream); break;
+            case 11008: lut2_launch_t<344>(p, X, out, stream); break;
+            case 14336: lut2_launch_t<448>(p, X, out, stream); break;
+            case 28672: lut2_launch_t<896>(p, X, out, stream); break;
+            default: lut2_launch_t<0>(p, X, out, stream); break;
+        }
+        note_launch();
+        BD_CUDA(cudaGetLastError());
         return;
     }
     // compile-time row strides for the published shapes (immediate load offsets)
