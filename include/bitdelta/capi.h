@@ -124,6 +124,14 @@ int bd_multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int3
                           int32_t batch, const int32_t* req_tenant, const void* X, float* Y,
                           void* stream);
 
+/* The same linear in f32 (W, X device f32; BASELINE configs[0], the reference's own
+ * precision, 1e-5 tolerance): K5, a SIMT kernel with fp64 accumulation — tcgen05 has
+ * no f32 kind. Rounds like the reference: Y = float(W x) + alpha * float(S x). */
+int bd_multitenant_linear_f32(const float* W, uint64_t out_dim, uint64_t in_dim, int32_t n_tenants,
+                              const uint8_t* const* tenant_bits, const float* tenant_alpha,
+                              int32_t batch, const int32_t* req_tenant, const float* X, float* Y,
+                              void* stream);
+
 /* ------------------------------------------------------------- serving -- */
 /* Device-resident ServingPool (P:include/deltakit/serve.hpp:59-100,
  * P:src/serve.cpp:93-325). Backbone linears are held in bf16, norms/embed in
@@ -215,6 +223,9 @@ typedef struct bd_pool_stats {
     double last_cold_load_ms; /* serve.hpp:79 */
     uint64_t resident_bytes;  /* device bytes: backbone + resident deltas + KV */
     uint64_t kernels_last_step; /* kernels launched by the last decode step */
+    char delta_paths[8];        /* K3 variant per projection group (q/k/v, o, gate/up, down) of
+                                   the last step: T = K23, L = byte LUT, X = K3t, F = i8 fused,
+                                   U = SIMT units; NUL-terminated */
 } bd_pool_stats;
 int bd_pool_get_stats(const bd_pool* pool, bd_pool_stats* out);
 

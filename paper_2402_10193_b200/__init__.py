@@ -150,10 +150,15 @@ def packed_matvec(bits, alpha: float, rows: int, cols: int, x, stream=None):
 
 
 def multitenant_linear(W, tenant_bits, tenant_alpha, req_tenant, X, stream=None):
-    """Y[b] = X[b] W^T + alpha[t(b)] S_t(b) X[b]   (bf16 W/X on device, f32 Y)."""
+    """Y[b] = X[b] W^T + alpha[t(b)] S_t(b) X[b]   (f32 Y).
+
+    bf16 W/X: K2 (tcgen05) + the K3 variants; f32 W/X: K5 (SIMT, fp64 accumulation,
+    the reference's own precision — BASELINE configs[0])."""
     import torch
 
     _req_cuda(W, X)
+    if W.dtype != X.dtype or W.dtype not in (torch.bfloat16, torch.float32):
+        raise BitDeltaError(5, "multitenant_linear: W and X must both be bf16 or both f32")
     out_dim, in_dim = W.shape
     B = X.shape[0]
     T = len(tenant_bits)
@@ -161,8 +166,8 @@ def multitenant_linear(W, tenant_bits, tenant_alpha, req_tenant, X, stream=None)
     alpha_arr = (C.c_float * max(T, 1))(*[float(a) for a in tenant_alpha])
     req_arr = (C.c_int32 * B)(*[int(t) for t in req_tenant])
     Y = torch.empty((B, out_dim), dtype=torch.float32, device=X.device)
-    check(lib().bd_multitenant_linear(_ptr(W), out_dim, in_dim, T, bits_arr, alpha_arr, B, req_arr,
-                                      _ptr(X), _ptr(Y), _stream(stream)))
+    fn = lib().bd_multitenant_linear_f32 if W.dtype == torch.float32 else lib().bd_multitenant_linear
+    check(fn(_ptr(W), out_dim, in_dim, T, bits_arr, alpha_arr, B, req_arr, _ptr(X), _ptr(Y), _stream(stream)))
     return Y
 
 

@@ -55,13 +55,13 @@ class Request(C.Structure):
 
 class PoolStats(C.Structure):
     _fields_ = [("backbone_passes", u64), ("cold_loads", u64), ("last_cold_load_ms", C.c_double),
-                ("resident_bytes", u64), ("kernels_last_step", u64)]
+                ("resident_bytes", u64), ("kernels_last_step", u64), ("delta_paths", C.c_char * 8)]
 
 
 SYMBOLS = [
     "bd_abi_version", "bd_last_error", "bd_device_check", "bd_launch_count", "bd_packed_size",
     "bd_compress", "bd_compress_batched", "bd_compress_stack", "bd_packed_signed_accumulate",
-    "bd_packed_matvec", "bd_multitenant_linear", "bd_pool_create", "bd_pool_destroy",
+    "bd_packed_matvec", "bd_multitenant_linear", "bd_multitenant_linear_f32", "bd_pool_create", "bd_pool_destroy",
     "bd_pool_set_tensor", "bd_pool_register_delta", "bd_pool_register_delta_file",
     "bd_pool_open_request", "bd_pool_close_request", "bd_pool_decode_step",
     "bd_pool_decode_layers", "bd_pool_get_stats", "bd_pool_profile_layers", "bd_nccl_unique_id",
@@ -87,6 +87,7 @@ def lib() -> C.CDLL:
     L.bd_packed_matvec.argtypes = [vp, C.c_float, u64, u64, vp, u64, vp, vp]
     L.bd_multitenant_linear.argtypes = [vp, u64, u64, C.c_int32, C.POINTER(vp), C.POINTER(C.c_float),
                                         C.c_int32, C.POINTER(C.c_int32), vp, vp, vp]
+    L.bd_multitenant_linear_f32.argtypes = L.bd_multitenant_linear.argtypes
     L.bd_pool_create.argtypes = [C.POINTER(Arch), C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
     L.bd_pool_destroy.argtypes = [vp]
     L.bd_pool_destroy.restype = None

@@ -460,6 +460,30 @@ int bd_multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int3
     });
 }
 
+int bd_multitenant_linear_f32(const float* W, uint64_t out_dim, uint64_t in_dim, int32_t n_tenants,
+                              const uint8_t* const* tenant_bits, const float* tenant_alpha,
+                              int32_t batch, const int32_t* req_tenant, const float* X, float* Y,
+                              void* stream) {
+    return guarded([&] {
+        require(W && X && Y, BD_ERR_BAD_ARGUMENT, "multitenant_linear_f32: null pointer");
+        require(batch >= 1 && batch <= 256, BD_ERR_BAD_ARGUMENT, "multitenant_linear_f32: batch must be 1..256");
+        require(out_dim >= 1 && in_dim >= 1, BD_ERR_BAD_ARGUMENT, "multitenant_linear_f32: empty matrix");
+        std::vector<const uint8_t*> rb(batch, nullptr);
+        std::vector<float> ra(batch, 0.0f);
+        for (int b = 0; b < batch; ++b) {
+            const int t = req_tenant ? req_tenant[b] : -1;
+            require(t < n_tenants, BD_ERR_UNKNOWN_ID, "multitenant_linear_f32: request tenant out of range");
+            if (t < 0) continue;
+            require(tenant_bits && tenant_alpha && tenant_bits[t], BD_ERR_BAD_ARGUMENT,
+                    "multitenant_linear_f32: missing tenant bits");
+            rb[b] = tenant_bits[t];
+            ra[b] = tenant_alpha[t];
+        }
+        f32_linear_launch(W, out_dim, in_dim, rb.data(), ra.data(), batch, X, Y,
+                          static_cast<cudaStream_t>(stream));
+    });
+}
+
 int bd_pool_create(const bd_arch* arch, int device, int world_size, int rank, bd_pool** out) {
     return guarded([&] {
         require(arch && out, BD_ERR_BAD_ARGUMENT, "pool_create: null argument");

@@ -195,6 +195,12 @@ struct MxdParams {
 bool plan_mxd(MxdParams& p, const int* seg_rows, int n_segs, int cols, int batch);
 void mxd_launch(const MxdParams& p, float* out, cudaStream_t stream);
 
+// ---- K5: fp32 multi-tenant linear (SIMT, fp64 accumulation; packed.cu) ----
+// Y[b] = W x_b + alpha_b S_b x_b for every b < batch (req_bits[b] == null: base only);
+// W f32 [rows x cols], X f32 [batch x cols], Y f32 [batch x rows]
+void f32_linear_launch(const float* W, uint64_t rows, uint64_t cols, const uint8_t* const* req_bits,
+                       const float* req_alpha, int batch, const float* X, float* Y, cudaStream_t stream);
+
 // Y[b][m] = sum_s P[s][b][m] (+ D[b][m])
 void combine_launch(const float* P, int splits, const float* D, int batch, int M, float* Y,
                     cudaStream_t stream, int dsplits = 1);

@@ -171,7 +171,108 @@ __global__ void combine_kernel(const float* __restrict__ P, int splits, const fl
     }
 }
 
+// ------------------------------------------------------------------ K5 --
+// fp32 multi-tenant linear (BASELINE configs[0]: the reference's f32 path at 1e-5):
+//   Y[b][r] = float(sum_j W[r][j] x_b[j]) + alpha_t(b) * float(sum_j s_t(b)[r][j] x_b[j])
+// mirroring matmul_nt (P:src/matrix.cpp:26-41) then apply_delta_correction's
+// y += alpha * packed_signed_accumulate (P:src/serve.cpp:19-36, delta.cpp:80-103), with
+// fp64 accumulation of both sums (the reference rounds a sequential f32 / f64 sum).
+// tcgen05 has no f32 kind, so this is a SIMT kernel; it is HBM-bound on W (4 B/weight,
+// read once for up to kF32Req requests) plus each request's tenant plane.
+// Warp per row, lane l covers columns [c0 + 4l, c0 + 4l + 4) of every 128-column step.
+constexpr int kF32Threads = 256;
+constexpr int kF32Req = 8;  // requests per pass over W
+struct F32Linear {
+    const float* W;
+    const float* X;  // [batch][cols]
+    float* Y;        // [batch][rows]
+    uint64_t rows, cols;
+    int batch;
+    int n_req;  // requests in this pass
+    int req[kF32Req];
+    const uint8_t* bits[kF32Req];  // tenant plane of each request (null = base only)
+    float alpha[kF32Req];
+};
+
+__global__ void __launch_bounds__(kF32Threads) f32_linear_kernel(const __grid_constant__ F32Linear a) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warps = uint64_t(gridDim.x) * (kF32Threads / 32);
+    const bool vec = (a.cols % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.W) | reinterpret_cast<uintptr_t>(a.X)) % 16 == 0);
+    for (uint64_t r = uint64_t(blockIdx.x) * (kF32Threads / 32) + (threadIdx.x >> 5); r < a.rows; r += warps) {
+        double base[kF32Req], del[kF32Req];
+#pragma unroll
+        for (int q = 0; q < kF32Req; ++q) base[q] = del[q] = 0.0;
+        const float* wr = a.W + r * a.cols;
+        const uint64_t nbytes = (a.rows * a.cols + 7) / 8;
+        for (uint64_t c = 4 * lane; c < a.cols; c += 128) {
+            float w[4];
+            const int take = a.cols - c < 4 ? int(a.cols - c) : 4;
+            if (vec) {
+                const float4 v = __ldcs(reinterpret_cast<const float4*>(wr + c));
+                w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) w[k] = k < take ? wr[c + k] : 0.0f;
+            }
+#pragma unroll
+            for (int q = 0; q < kF32Req; ++q) {
+                if (q >= a.n_req) break;
+                const float* xr = a.X + size_t(a.req[q]) * a.cols + c;
+                float x[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) x[k] = k < take ? __ldg(xr + k) : 0.0f;
+                uint32_t sb = 0;
+                if (a.bits[q]) sb = bit_window(a.bits[q], nbytes, r * a.cols + c);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    base[q] = fma(double(w[k]), double(x[k]), base[q]);
+                    if (k < take) del[q] += ((sb >> k) & 1u) ? double(x[k]) : -double(x[k]);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kF32Req; ++q) {
+            if (q >= a.n_req) break;
+            double b = base[q], d = del[q];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                b += __shfl_xor_sync(0xffffffffu, b, o);
+                d += __shfl_xor_sync(0xffffffffu, d, o);
+            }
+            if (lane == 0) {
+                float y = float(b);
+                if (a.bits[q]) y = y + a.alpha[q] * float(d);
+                a.Y[size_t(a.req[q]) * a.rows + r] = y;
+            }
+        }
+    }
+}
+
 }  // namespace
+
+void f32_linear_launch(const float* W, uint64_t rows, uint64_t cols, const uint8_t* const* req_bits,
+                       const float* req_alpha, int batch, const float* X, float* Y, cudaStream_t stream) {
+    if (rows == 0 || batch == 0) return;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((rows + 7) / 8, kNumSMs * 8));
+    for (int first = 0; first < batch; first += kF32Req) {
+        F32Linear a{};
+        a.W = W;
+        a.X = X;
+        a.Y = Y;
+        a.rows = rows;
+        a.cols = cols;
+        a.batch = batch;
+        a.n_req = std::min(kF32Req, batch - first);
+        for (int q = 0; q < a.n_req; ++q) {
+            a.req[q] = first + q;
+            a.bits[q] = req_bits[first + q];
+            a.alpha[q] = req_alpha[first + q];
+        }
+        f32_linear_kernel<<<grid, kF32Threads, 0, stream>>>(a);
+        note_launch();
+        BD_CUDA(cudaGetLastError());
+    }
+}
 
 void packed_accumulate_launch(const uint8_t* bits, uint64_t rows, uint64_t cols, const float* x,
                               uint64_t n_vec, float* out, float scale, bool overwrite,

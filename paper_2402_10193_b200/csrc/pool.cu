@@ -1380,7 +1380,23 @@ struct PoolImpl {
                       logits, s);
     }
 
+    // K3 variant per projection group (q/k/v, o, gate/up, down) of layer 0 of plan p:
+    // T = K23 (FP4 tensor cores, fused with K2), L = byte LUT beside K2, X = K3t beside K2,
+    // F = i8 tensor-core fused kernel, U = SIMT units
+    void record_paths(const Plan& p) {
+        for (int gi = 0; gi < 4; ++gi) {
+            char c = 'U';
+            if (a.n_layers == 0) c = '-';
+            else if (mt4_ok(p, 0, gi)) c = 'T';
+            else if (lut_ok(p, 0, gi)) c = p.lut[0][gi].mxd ? 'X' : 'L';
+            else if (fused_ok(p, 0, gi)) c = 'F';
+            stats.delta_paths[gi] = c;
+        }
+        stats.delta_paths[4] = 0;
+    }
+
     void execute(Plan& p, bool full) {
+        record_paths(p);
         cudaGraphExec_t& g = full ? p.graph_full : p.graph_layers;
         uint64_t& kcount = full ? p.kernels_full : p.kernels_layers;
         if (!use_graphs) {

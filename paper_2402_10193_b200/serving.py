@@ -182,7 +182,7 @@ class ServingPool:
         check(lib().bd_pool_get_stats(self._h, C.byref(st)))
         return {"backbone_passes": st.backbone_passes, "cold_loads": st.cold_loads,
                 "last_cold_load_ms": st.last_cold_load_ms, "resident_bytes": st.resident_bytes,
-                "kernels_last_step": st.kernels_last_step}
+                "kernels_last_step": st.kernels_last_step, "delta_paths": st.delta_paths.decode()}
 
     def resident_bytes(self) -> int:
         return self.stats()["resident_bytes"]

@@ -11,6 +11,8 @@ Outputs (committed, small):
                         for the test_serve.cpp universe (kCfg, seeds 1001 / 2000+i)
   toy_decode.npz        backbone (synth_base), token streams and the reference
                         ServingPool shared-mode logits for B in {1,2,4}
+  mp_t*.bdelta, mp_decode.npz (--mp)  2- and 3-plane deltas on a 256-dim config
+                        written by the reference, and its logits for B in {4,16}
 """
 from __future__ import annotations
 
@@ -96,5 +98,38 @@ def main():
     print("golden fixtures written to", HERE)
 
 
+# multi-plane universe on a 128-multiple shape (the byte-LUT / K23 paths; the toy above
+# only reaches the SIMT units): tenants with 2 and 3 sign planes per projection
+# (compress_stack, P:src/delta.cpp:57-70; --bits k of P:tools/main.cpp:455-460)
+MP_CFG = {"vocab": 64, "dim": 256, "n_layers": 1, "n_heads": 2, "intermediate": 512, "max_seq": 16,
+          "rope_theta": 10000.0}
+MP_PLANES = [2, 3, 3, 2]
+
+
+def mp_universe():
+    r = oracle.ref()
+    cfg = json.dumps(MP_CFG)
+    base = r.synth_base(cfg, 3003, 0.08)
+    for i, k in enumerate(MP_PLANES):
+        fine = r.synth_fine(cfg, base, 0.03, 4000 + i)
+        r.write_delta_file(cfg, base, fine, k, os.path.join(HERE, f"mp_t{i}.bdelta"))
+    d = {"cfg": np.array(cfg), "base": base}
+    # B = 4: one request per tenant; B = 16: four per tenant (the K23 slots)
+    for B in (4, 16):
+        pool = r.pool(cfg, base)
+        for i in range(len(MP_PLANES)):
+            pool.register_delta(f"t{i}", os.path.join(HERE, f"mp_t{i}.bdelta"))
+        rids = [pool.open_request(f"t{i % len(MP_PLANES)}") for i in range(B)]
+        stream = np.random.default_rng(77 + B).integers(0, MP_CFG["vocab"], 4).astype(np.int32)
+        logits = [pool.decode_step([(rid, int(tok), pos) for rid in rids]) for pos, tok in enumerate(stream)]
+        d[f"B{B}_tokens"] = stream
+        d[f"B{B}_logits"] = np.stack(logits)
+    np.savez_compressed(os.path.join(HERE, "mp_decode.npz"), **d)
+    print("multi-plane fixtures written to", HERE)
+
+
 if __name__ == "__main__":
-    main()
+    if "--mp" in sys.argv:
+        mp_universe()
+    else:
+        main()

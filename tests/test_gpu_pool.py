@@ -378,3 +378,24 @@ print('ok')
     env = dict(os.environ, BD_DELTA="mt4")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("B,paths", [(4, "LLLL"), (16, "TTTT")])
+def test_multi_plane_reference_bdelta(cuda, B, paths):
+    """2- and 3-plane .bdelta files written by the reference (make_golden.py --mp) served
+    through the byte LUT (1 request per tenant) and K23 (4 per tenant), against the
+    reference ServingPool's logits (f32) within the bf16 tolerance."""
+    d = np.load(os.path.join(GOLDEN, "mp_decode.npz"))
+    arch = dict(json.loads(str(d["cfg"])))
+    arch["kv_dim"] = arch["dim"]
+    pool = ServingPool(arch, tensors_of(arch, d["base"]))
+    for i in range(4):
+        pool.register_delta(f"t{i}", os.path.join(GOLDEN, f"mp_t{i}.bdelta"))
+    rids = [pool.open_request(f"t{i % 4}") for i in range(B)]
+    for pos, tok in enumerate(d[f"B{B}_tokens"]):
+        got = pool.decode_step([(r, int(tok), pos) for r in rids])
+        assert pool.stats()["delta_paths"] == paths
+        want = d[f"B{B}_logits"][pos]
+        for i in range(B):
+            assert rel_l2(got[i], want[i]) <= 1e-2, (pos, i, rel_l2(got[i], want[i]))
+    pool.close()
