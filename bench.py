@@ -49,6 +49,21 @@ WORKLOADS = {
     "m7_stack": dict(arch=dict(vocab=32000, dim=4096, kv_dim=1024, n_layers=32, n_heads=32,
                                intermediate=14336), tenants=16, batch=64, ctx=128),
 }
+# configs[4]: Llama-2-70B (GQA, 28672 FFN), 32 tenants, batch 32; 80 layers need the 8-GPU
+# row sharding (--layers N runs a shorter stack on fewer GPUs)
+WORKLOADS["l70_stack"] = dict(arch=dict(vocab=32000, dim=8192, kv_dim=1024, n_layers=80, n_heads=64,
+                                        intermediate=28672), tenants=32, batch=32, ctx=128)
+# K1 compressor workloads (a step = one compress pass; metric GB/s of algorithmic bytes,
+# (2 s_in + 1/8) B per parameter):
+#   compress_f32: configs[0], one 4096 x 4096 f32 base / fine-tune pair (L2 flushed per step);
+#   compress_l70: configs[4]'s compression, one tenant's 7 projection matrices of --layers
+#                 Llama-2-70B layers (bf16) per step, one batched launch; N GPUs compress
+#                 disjoint layer ranges (no exchange: weak scaling)
+COMPRESS = {
+    "compress_f32": dict(shapes=[(4096, 4096)], dtype="f32", layers=1),
+    "compress_l70": dict(shapes=[(8192, 8192), (1024, 8192), (1024, 8192), (8192, 8192), (28672, 8192),
+                                 (28672, 8192), (8192, 28672)], dtype="bf16", layers=2),
+}
 PROJ = ["attn_q", "attn_k", "attn_v", "attn_o", "mlp_gate", "mlp_up", "mlp_down"]
 PROF_KINDS = ["gemm_qkv", "gemm_o", "gemm_gu", "gemm_down", "delta_qkv", "delta_o", "delta_gu",
               "delta_down", "attn", "norm", "silu", "fused_qkv", "fused_o", "fused_gu", "fused_down",
@@ -202,8 +217,8 @@ def run_ours(args, rank, world, dev):
 
     wl = WORKLOADS[args.workload]
     arch = dict(wl["arch"], rope_theta=10000.0)
-    if os.environ.get("BD_BENCH_INTER"):  # shape experiments only (not a BASELINE config)
-        arch["intermediate"] = int(os.environ["BD_BENCH_INTER"])
+    if args.layers:
+        arch["n_layers"] = args.layers
     T = args.tenants or wl["tenants"]
     B = args.batch or wl["batch"]
     ctx = args.ctx or wl["ctx"]
@@ -328,6 +343,147 @@ def roofline(res, hbm_peak, peak_kind):
             "share_of_step": round(cand[dom]["ms"] / total_ms, 4) if total_ms else None}
 
 
+# ------------------------------------------------------------ compression --
+def run_compress(args, rank, world, dev):
+    """K1 over fine-tune / base pairs resident in HBM; CUDA events around K steps."""
+    import torch
+
+    import paper_2402_10193_b200 as bd
+
+    wl = COMPRESS[args.workload]
+    f32 = wl["dtype"] == "f32"
+    dt = torch.float32 if f32 else torch.bfloat16
+    layers = args.layers or wl["layers"]
+    g = torch.Generator(device=dev).manual_seed(77 + rank)
+    pairs = []
+    for _ in range(layers):
+        for rows, cols in wl["shapes"]:
+            base = (torch.randn(rows, cols, device=dev, generator=g) * 0.02).to(dt)
+            fine = (base.float() + torch.randn(rows, cols, device=dev, generator=g) * 1e-3).to(dt)
+            pairs.append((base, fine))
+    params = sum(b.numel() for b, _ in pairs)
+    s_in = 4 if f32 else 2
+    algo = params * (2 * s_in + 1 / 8) + 4 * len(pairs)
+    outs = [(torch.empty(bd.packed_size(*b.shape), dtype=torch.uint8, device=dev),
+             torch.empty(1, dtype=torch.float32, device=dev)) for b, _ in pairs]
+    # inputs below ~4x L2: read a 512 MB buffer between steps (a read leaves clean lines, so
+    # no write-back of flush data lands inside the timed kernel)
+    flush = torch.ones(128 << 20, dtype=torch.float32, device=dev) if algo < 512e6 else None
+
+    def step():
+        bd.compress_batched(pairs, outs=outs)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist_barrier(world)
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = bd.launch_count()
+    with ClockSampler(dev.index or 0) as clk:
+        torch.cuda.synchronize()
+        clk.mark("t0")
+        for a, b in ev:
+            if flush is not None:
+                flush.sum()  # evict the inputs from L2 (read-only sweep)
+            a.record(stream)
+            step()
+            b.record(stream)
+        torch.cuda.synchronize()
+        clk.mark("t1")
+    launches = bd.launch_count() - launches0
+    dist_barrier(world)
+    ms = dist_max(sum(a.elapsed_time(b) for a, b in ev), world, dev)
+    ms_step = ms / args.steps
+    # e2e through the public API: host (pinned) pairs in, packed bits + alpha out, per step
+    hp = [(b.cpu().pin_memory(), f.cpu().pin_memory()) for b, f in pairs]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dpairs = [(torch.empty_like(b), torch.empty_like(f)) for b, f in pairs]
+    hout = [torch.empty(o.numel(), dtype=torch.uint8).pin_memory() for o, _ in outs]
+    e_steps = min(args.steps, 4)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(e_steps):
+        for (db, df), (hb, hf) in zip(dpairs, hp):
+            db.copy_(hb, non_blocking=True)
+            df.copy_(hf, non_blocking=True)
+        bd.compress_batched(dpairs, outs=outs)
+        for (o, _), h in zip(outs, hout):
+            h.copy_(o, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = dist_max(e0.elapsed_time(e1), world, dev) / e_steps
+    # parity of the measured output against a torch restatement (first matrix)
+    b0, f0 = pairs[0]
+    d0 = (f0.float() - b0.float()).reshape(-1)
+    bits0 = outs[0][0]
+    ok = bool(torch.equal(bits0, _torch_pack(d0)))
+    hbm, _, kind = peaks()
+    gbs = world * algo / (ms_step / 1e3) / 1e9
+    line = {"metric": "delta compression (K1) GB/s of algorithmic bytes", "value": round(gbs, 1),
+            "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if f32 else "bf16",
+            "data": "synthetic (base N(0,0.02), fine = base + N(0,1e-3))",
+            "config": {"workload": args.workload, "matrices_per_gpu": len(pairs), "params_per_gpu": params,
+                       "layers_per_gpu": layers if not f32 else None,
+                       "l2": "flushed between steps (512 MB read sweep)" if flush is not None else "inputs > L2"},
+            "e2e": {"value": round(world * algo / (e2e_ms / 1e3) / 1e9, 1), "unit": "GB/s",
+                    "h2d_bytes_per_step": 2 * s_in * params, "d2h_bytes_per_step": sum(o.numel() for o, _ in outs)},
+            "gpu_launches": launches,
+            "roofline": {"kernel": "compress_kernel", "bound": "hbm", "achieved": round(algo / (ms_step / 1e3) / 1e9, 1),
+                         "peak": hbm, "peak_kind": kind, "unit": "GB/s",
+                         "frac": round(algo / (ms_step / 1e3) / 1e9 / hbm, 4), "traffic": None,
+                         "algorithmic_bytes_per_launch": algo, "avg_launch_ms": round(ms_step, 5),
+                         "share_of_step": 1.0},
+            "parity_first_matrix_bits_exact": ok,
+            "clocks": clk.summary()}
+    return line
+
+
+def _torch_pack(d):
+    import torch
+
+    v = (d > 0).to(torch.uint8)
+    pad = (-v.numel()) % 8
+    if pad:
+        v = torch.cat([v, torch.zeros(pad, dtype=torch.uint8, device=v.device)])
+    w = torch.tensor([1, 2, 4, 8, 16, 32, 64, 128], dtype=torch.int32, device=v.device)
+    return (v.view(-1, 8).to(torch.int32) * w).sum(1).to(torch.uint8)
+
+
+def cpu_reference_compress(budget_matrices=None):
+    """The reference compress_tensor (oracle/_ref) on 4096 x 4096 f32 pairs, all host threads
+    (one matrix per thread); GB/s of the same algorithmic bytes (2*4 + 1/8 B/param)."""
+    import ctypes as C
+
+    import numpy as np
+
+    import oracle
+
+    lib = oracle._ref_lib()
+    threads = os.cpu_count() or 1
+    n = budget_matrices or threads
+    rows = cols = 4096
+    rng = np.random.default_rng(0)
+    base = [(rng.standard_normal((rows, cols), dtype=np.float32) * 0.02) for _ in range(n)]
+    fine = [(b + rng.standard_normal((rows, cols), dtype=np.float32) * 1e-3).astype(np.float32) for b in base]
+    bits = [np.zeros(rows * cols // 8, np.uint8) for _ in range(n)]
+    fp = C.POINTER(C.c_float)
+    bp = (fp * n)(*[b.ctypes.data_as(fp) for b in base])
+    fpp = (fp * n)(*[f.ctypes.data_as(fp) for f in fine])
+    op = (C.POINTER(C.c_uint8) * n)(*[b.ctypes.data_as(C.POINTER(C.c_uint8)) for b in bits])
+    scales = np.zeros(n, np.float32)
+    secs = C.c_double()
+    rc = lib.dkref_time_compress(bp, fpp, C.c_uint64(n), C.c_uint64(rows), C.c_uint64(cols), C.c_uint64(threads),
+                                 op, scales.ctypes.data_as(fp), C.byref(secs))
+    assert rc == 0
+    algo = n * rows * cols * (2 * 4 + 1 / 8)
+    return {"value": round(algo / secs.value / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+            "sample": f"reference compress_tensor on {n} 4096x4096 f32 pairs, {threads} threads "
+                      f"({secs.value:.2f} s)"}
+
+
 # ------------------------------------------------------------------ cpu arm --
 def cpu_reference_tok_s(arch, T, B, budget_s=12.0):
     """Reference deltakit (oracle/_ref) on a bounded sample: the per-projection work
@@ -402,8 +558,10 @@ def run_reference(args):
 
 
 def config_of(args, arch, T, B, ctx):
-    return {"workload": args.workload, "model": "llama2-7b-shaped" if arch["kv_dim"] == arch["dim"] else
-            "mistral-7b-shaped", "layers": arch["n_layers"], "tenants": T, "global_batch": B * args.gpus,
+    model = ("llama2-70b-shaped" if arch["dim"] == 8192 else
+             "llama2-7b-shaped" if arch["kv_dim"] == arch["dim"] else "mistral-7b-shaped")
+    return {"workload": args.workload, "model": model, "layers": arch["n_layers"], "tenants": T,
+            "global_batch": B if args.parallelism == "tp" else B * args.gpus,
             "batch_per_gpu": B, "seq_len": ctx,
             "parallelism": (f"tp{args.gpus}" if args.parallelism == "tp" else f"replicas{args.gpus}")
             if args.gpus > 1 else "single",
@@ -429,27 +587,56 @@ def dist_max(v, world, dev):
     return float(t.item())
 
 
+def spawn_ranks(n):
+    """`python bench.py --gpus N` without a launcher: one process per GPU (what torchrun
+    would start), rendezvous on 127.0.0.1; rank 0 prints the line."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env))
+    return max(p.wait() for p in procs)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="l7_stack", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="l7_stack", choices=sorted(WORKLOADS) + sorted(COMPRESS))
+    ap.add_argument("--layers", type=int, default=0, help="override the workload's layer count")
     ap.add_argument("--tenants", type=int, default=0)
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--ctx", type=int, default=0, help="context length before timing (default: workload)")
-    ap.add_argument("--parallelism", default="replicas", choices=["replicas", "tp"],
-                    help="N>1: independent replicas (weak scaling) or one row-sharded pool over NCCL")
+    ap.add_argument("--parallelism", default="tp", choices=["replicas", "tp"],
+                    help="N>1: one row-sharded pool over NCCL (north star, strong scaling; default) or "
+                         "independent replicas (weak scaling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
         if rank == 0:
-            run_reference(args)
+            if args.workload in COMPRESS:
+                cb = cpu_reference_compress()
+                print(json.dumps({"impl": "reference", "metric": "delta compression (K1) GB/s of algorithmic bytes",
+                                  "value": cb["value"], "unit": "GB/s", "n_gpus": args.gpus, "steps": 1,
+                                  "warmup": 0, "higher_is_better": True, "dtype": "f32", "data": "synthetic",
+                                  "config": {"workload": args.workload}, "cpu_baseline": cb,
+                                  "e2e": {"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                                          "d2h_bytes_per_step": 0}}), flush=True)
+            else:
+                run_reference(args)
         return
 
     import torch
@@ -460,6 +647,17 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
+    if args.workload in COMPRESS:
+        line = run_compress(args, rank, world, dev)
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_reference_compress()
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+        return
     res = run_ours(args, rank, world, dev)
     hbm, tfl, kind = peaks()
     rl = roofline(res, hbm, kind)

@@ -155,6 +155,11 @@ void bd_pool_destroy(bd_pool* pool);
  * calls bd_pool_init_comm before registering deltas or decoding. */
 int bd_nccl_unique_id(void* id_out /* 128 bytes */);
 int bd_pool_init_comm(bd_pool* pool, const void* id /* 128 bytes */);
+/* Test hook (no reference counterpart): instead of NCCL, the world_size pools of ONE
+ * process on ONE device (each driven from its own host thread) exchange through device
+ * copies; every other part of the row-sharded path runs unchanged. Pools joining the
+ * same `group` name form one world. Decode then runs eagerly (no CUDA graph). */
+int bd_pool_init_loopback(bd_pool* pool, const char* group);
 
 /* Backbone tensor by reference name (arch.cpp:51-69: "embed",
  * "layers.{i}.{attn_q,...,norm2}", "final_norm", "lm_head"), full (unsharded)

@@ -83,12 +83,13 @@ def compress_delta(delta, stream=None):
     return compress_tensor(None, delta, stream)
 
 
-def compress_batched(pairs, stream=None):
-    """Many (base, fine) pairs of one dtype in a single launch; returns [(bits, alpha)]."""
+def compress_batched(pairs, stream=None, outs=None):
+    """Many (base, fine) pairs of one dtype in a single launch; returns [(bits, alpha)]
+    (written into `outs` when given: [(uint8[packed_size], f32[1])] per pair)."""
     import torch
 
     jobs = (CompressJob * len(pairs))()
-    outs, keep = [], []
+    given, outs, keep = outs, [], []
     dt = None
     for i, (b, f) in enumerate(pairs):
         _req_cuda(b, f)
@@ -98,8 +99,13 @@ def compress_batched(pairs, stream=None):
         if _dtype(f) != dt:
             raise BitDeltaError(5, "compress_batched: mixed dtypes")
         rows, cols = f.shape
-        bits = torch.empty(packed_size(rows, cols), dtype=torch.uint8, device=f.device)
-        alpha = torch.empty(1, dtype=torch.float32, device=f.device)
+        if given is not None:
+            bits, alpha = given[i]
+            if bits.numel() != packed_size(rows, cols) or not bits.is_cuda or not alpha.is_cuda:
+                raise BitDeltaError(8, "compress_batched: output buffer of the wrong size")
+        else:
+            bits = torch.empty(packed_size(rows, cols), dtype=torch.uint8, device=f.device)
+            alpha = torch.empty(1, dtype=torch.float32, device=f.device)
         jobs[i] = CompressJob(_ptr(b) or None, _ptr(f), rows, cols, _ptr(bits), _ptr(alpha))
         outs.append((bits, alpha))
         keep += [b, f]

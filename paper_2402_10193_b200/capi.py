@@ -65,7 +65,7 @@ SYMBOLS = [
     "bd_pool_set_tensor", "bd_pool_register_delta", "bd_pool_register_delta_file",
     "bd_pool_open_request", "bd_pool_close_request", "bd_pool_decode_step",
     "bd_pool_decode_layers", "bd_pool_get_stats", "bd_pool_profile_layers", "bd_nccl_unique_id",
-    "bd_pool_init_comm", "bd_trace_enable", "bd_trace_read",
+    "bd_pool_init_comm", "bd_pool_init_loopback", "bd_trace_enable", "bd_trace_read",
 ]
 
 
@@ -103,6 +103,7 @@ def lib() -> C.CDLL:
                                          C.POINTER(u64), vp]
     L.bd_nccl_unique_id.argtypes = [vp]
     L.bd_pool_init_comm.argtypes = [vp, vp]
+    L.bd_pool_init_loopback.argtypes = [vp, C.c_char_p]
     if hasattr(L, "bd_trace_enable"):  # diagnostics (absent from older builds used in A/B runs)
         L.bd_trace_enable.argtypes = [C.c_uint32]
         L.bd_trace_read.argtypes = [vp, C.c_uint32, C.POINTER(C.c_uint32)]

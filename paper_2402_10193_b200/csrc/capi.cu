@@ -78,6 +78,7 @@ void pool_profile_layers(bd_pool* p, const bd_request* r, uint64_t n, const floa
                          float* xout, double* ms, uint64_t* cnt, void* s);
 void nccl_unique_id(void* out);
 void pool_init_comm(bd_pool* p, const void* id);
+void pool_init_loopback(bd_pool* p, const char* group);
 
 template <class F>
 int guarded(F&& f) {
@@ -503,6 +504,13 @@ int bd_pool_init_comm(bd_pool* pool, const void* id) {
     return guarded([&] {
         require(pool && id, BD_ERR_BAD_ARGUMENT, "init_comm: null argument");
         pool_init_comm(pool, id);
+    });
+}
+
+int bd_pool_init_loopback(bd_pool* pool, const char* group) {
+    return guarded([&] {
+        require(pool, BD_ERR_BAD_ARGUMENT, "init_loopback: null pool");
+        pool_init_loopback(pool, group);
     });
 }
 int bd_pool_set_tensor(bd_pool* pool, const char* name, const void* data, bd_dtype dtype,

@@ -23,7 +23,19 @@ namespace bd {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kVecPerThread = 4;  // 16-byte loads per tensor per thread per chunk
+// 16-byte loads per tensor per thread per block, issued in groups of kLoadGroup (8 loads of
+// 16 B in flight per thread). Measured on B200 (tools/k1_var.sh, profiles/r02_exp_k1_vpt.txt):
+// bf16 L70 layer set 3.5 / 5.7 / 5.2 / 3.0 TB/s at 4 / 8 / 16 / 32 -> 8 for bf16 (64 KB of
+// input per block); f32 4096^2 best at 4.
+#ifndef BD_K1_VPT_BF16
+#define BD_K1_VPT_BF16 8
+#endif
+#ifndef BD_K1_VPT_F32
+#define BD_K1_VPT_F32 4
+#endif
+template <bool kBf16>
+constexpr int kVecPerThread = kBf16 ? BD_K1_VPT_BF16 : BD_K1_VPT_F32;
+constexpr int kLoadGroup = 4;
 constexpr int kMaxJobsPerLaunch = 192;
 
 struct Job {
@@ -90,7 +102,7 @@ template <bool kBf16>
 __global__ void __launch_bounds__(kThreads) compress_kernel(const __grid_constant__ JobTable tab) {
     using E = Elt<kBf16>;
     constexpr int P = E::kPerVec;              // elements per 16-byte vector
-    constexpr int kChunk = kThreads * kVecPerThread * P;  // elements per block
+    constexpr int kChunk = kThreads * kVecPerThread<kBf16> * P;  // elements per block
     __shared__ double s_red[kThreads / 32];
     __shared__ bool s_last;
 
@@ -110,22 +122,8 @@ __global__ void __launch_bounds__(kThreads) compress_kernel(const __grid_constan
 
     // warp-span layout: each iteration a warp covers 32*P consecutive elements
     // (lane l holds elements l*P .. l*P+P-1 of the span).
-#pragma unroll
-    for (int it = 0; it < kVecPerThread; ++it) {
+    auto process = [&](int it, const float (&f)[P], const float (&b)[P]) {
         const uint64_t span0 = blk * kChunk + (uint64_t(it) * (kThreads / 32) + warp) * 32 * P;
-        const uint64_t e0 = span0 + lane * P;
-        float f[P], b[P];
-        if (vec_ok && e0 + P <= n) {
-            E::load_vec(job.fine, e0, f);
-            if (job.base) E::load_vec(job.base, e0, b);
-        } else {
-#pragma unroll
-            for (int k = 0; k < P; ++k) {
-                const bool in = e0 + k < n;
-                f[k] = in ? E::load(job.fine, e0 + k) : 0.0f;
-                b[k] = (in && job.base) ? E::load(job.base, e0 + k) : 0.0f;
-            }
-        }
         uint32_t mybits = 0;
 #pragma unroll
         for (int k = 0; k < P; ++k) {
@@ -141,6 +139,36 @@ __global__ void __launch_bounds__(kThreads) compress_kernel(const __grid_constan
         if (lane % kLanesPerWord == 0) {
             const uint64_t word_idx = span0 / 32 + lane / kLanesPerWord;
             if (word_idx * 32 < n) store_word(job.bits, word_idx, w, nbytes, bits_aligned);
+        }
+    };
+    auto e0_of = [&](int it) {
+        return blk * kChunk + (uint64_t(it) * (kThreads / 32) + warp) * 32 * P + lane * P;
+    };
+#pragma unroll 1
+    for (int it0 = 0; it0 < kVecPerThread<kBf16>; it0 += kLoadGroup) {
+        if (vec_ok && e0_of(it0 + kLoadGroup - 1) + P <= n) {
+            // fast path: all 2 x kLoadGroup 16-byte loads issued before any is consumed
+            float f[kLoadGroup][P], b[kLoadGroup][P];
+#pragma unroll
+            for (int g = 0; g < kLoadGroup; ++g) {
+                E::load_vec(job.fine, e0_of(it0 + g), f[g]);
+                if (job.base) E::load_vec(job.base, e0_of(it0 + g), b[g]);
+            }
+#pragma unroll
+            for (int g = 0; g < kLoadGroup; ++g) process(it0 + g, f[g], b[g]);
+        } else {
+#pragma unroll 1
+            for (int g = 0; g < kLoadGroup; ++g) {
+                const uint64_t e0 = e0_of(it0 + g);
+                float f[P], b[P];
+#pragma unroll
+                for (int k = 0; k < P; ++k) {
+                    const bool in = e0 + k < n;
+                    f[k] = in ? E::load(job.fine, e0 + k) : 0.0f;
+                    b[k] = (in && job.base) ? E::load(job.base, e0 + k) : 0.0f;
+                }
+                process(it0 + g, f, b);
+            }
         }
     }
 
@@ -207,7 +235,7 @@ void compress_launch(const bd_compress_job* jobs, int n_jobs, bd_dtype dtype,
     require(dtype == BD_F32 || dtype == BD_BF16, BD_ERR_UNSUPPORTED_DTYPE,
             "compress: dtype must be BD_F32 or BD_BF16");
     const bool bf16 = dtype == BD_BF16;
-    const uint64_t chunk = uint64_t(kThreads) * kVecPerThread * (bf16 ? 8 : 4);
+    const uint64_t chunk = uint64_t(kThreads) * (bf16 ? kVecPerThread<true> * 8 : kVecPerThread<false> * 4);
     for (int first = 0; first < n_jobs; first += kMaxJobsPerLaunch) {
         const int cnt = std::min(kMaxJobsPerLaunch, n_jobs - first);
         JobTable tab{};

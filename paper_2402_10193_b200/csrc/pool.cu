@@ -21,8 +21,10 @@
 #include <array>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <string>
 #include <vector>
@@ -61,6 +63,33 @@ __global__ void f32_to_bf16_2d(const float* __restrict__ src, uint64_t rows, uin
 }
 
 uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
+
+// Test hook (bd_pool_init_loopback): the row-sharded pools of one process on ONE device,
+// each driven from its own host thread, exchange through device copies instead of NCCL
+// (NCCL refuses two ranks on one GPU). Every other part of the tensor-parallel path (rank
+// row slices, head-local attention, shard_reduce, gather_transpose) runs as with NCCL.
+struct LoopbackGroup {
+    int world = 0;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t gen = 0;
+    std::vector<void*> recv;
+    std::vector<cudaEvent_t> ready, done;
+    void barrier() {
+        std::unique_lock<std::mutex> lk(m);
+        const uint64_t g = gen;
+        if (++arrived == world) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+std::mutex g_loop_m;
+std::map<std::string, std::shared_ptr<LoopbackGroup>> g_loop_groups;
 
 template <typename T>
 T* dmalloc(size_t n, std::vector<void*>* owner = nullptr) {
@@ -183,6 +212,8 @@ struct PoolImpl {
     void* msq = nullptr;  // RMSNorm workspace (norm_ws_bytes: arrival counters + chunk sums)
     // tensor parallel (world > 1)
     ncclComm_t comm = nullptr;
+    std::shared_ptr<LoopbackGroup> loop;  // test hook instead of comm (bd_pool_init_loopback)
+    cudaEvent_t lb_ready = nullptr, lb_done = nullptr;
     uint16_t *ctx_loc = nullptr, *act_loc = nullptr, *gath16 = nullptr;
     float *red_loc = nullptr, *gath32 = nullptr;
     uint16_t *xn = nullptr, *ctx = nullptr, *act = nullptr;
@@ -217,6 +248,8 @@ struct PoolImpl {
         if (ev_join) cudaEventDestroy(ev_join);
         if (stream2) cudaStreamDestroy(stream2);
         if (comm) ncclCommDestroy(comm);
+        if (lb_ready) cudaEventDestroy(lb_ready);
+        if (lb_done) cudaEventDestroy(lb_done);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -1306,15 +1339,37 @@ struct PoolImpl {
     // residual stream entering layer 0 and leaves it after the last layer
     // ---- tensor-parallel exchanges (world > 1): NCCL all-gather over NVLink ----
     // bf16 activation slice [B x n_l] -> every rank's slices -> [B x ld] in column order
+    void all_gather(const void* send, void* recv, size_t cnt, ncclDataType_t dt, size_t elem, cudaStream_t s) {
+        if (!loop) {
+            BD_NCCL(ncclAllGather(send, recv, cnt, dt, comm, s));
+            return;
+        }
+        LoopbackGroup& G = *loop;
+        const size_t bytes = cnt * elem;
+        G.recv[rank] = recv;
+        BD_CUDA(cudaEventRecord(lb_ready, s));  // this rank's earlier readers of recv are done
+        G.ready[rank] = lb_ready;
+        G.barrier();
+        for (int q = 0; q < world; ++q) {
+            BD_CUDA(cudaStreamWaitEvent(s, G.ready[q], 0));
+            BD_CUDA(cudaMemcpyAsync(static_cast<char*>(G.recv[q]) + rank * bytes, send, bytes,
+                                    cudaMemcpyDeviceToDevice, s));
+        }
+        BD_CUDA(cudaEventRecord(lb_done, s));
+        G.done[rank] = lb_done;
+        G.barrier();
+        for (int q = 0; q < world; ++q) BD_CUDA(cudaStreamWaitEvent(s, G.done[q], 0));
+        G.barrier();  // all waits enqueued before any rank re-records its events
+    }
     void exchange_bf16(const uint16_t* local, int B, int n_l, uint16_t* full, int ld, cudaStream_t s) {
         const size_t cnt = size_t(B) * n_l;
-        BD_NCCL(ncclAllGather(local, gath16, cnt, ncclBfloat16, comm, s));
+        all_gather(local, gath16, cnt, ncclBfloat16, 2, s);
         gather_transpose_launch(gath16, world, B, n_l, full, ld, s);
     }
     // row-sharded f32 projection output -> gathered view consumed by the residual kernel
     ProjOut exchange_f32(const ProjOut& part, int B, int n_l, cudaStream_t s) {
         shard_reduce_launch(part, B, n_l, red_loc, s);
-        BD_NCCL(ncclAllGather(red_loc, gath32, size_t(B) * n_l, ncclFloat32, comm, s));
+        all_gather(red_loc, gath32, size_t(B) * n_l, ncclFloat32, 4, s);
         ProjOut g;
         g.G = gath32;
         g.g_cols = n_l;
@@ -1499,7 +1554,7 @@ struct PoolImpl {
         validate(reqs, n);
         if (n == 0) return;
         require(n <= 256, BD_ERR_BAD_ARGUMENT, "decode: batch must be <= 256");
-        require(world == 1 || comm != nullptr, BD_ERR_BAD_ARGUMENT,
+        require(world == 1 || comm != nullptr || loop != nullptr, BD_ERR_BAD_ARGUMENT,
                 "decode: world_size > 1 needs bd_pool_init_comm first");
         std::vector<int> idx(n);
         for (uint64_t i = 0; i < n; ++i) {
@@ -1650,6 +1705,32 @@ void pool_init_comm(bd_pool* p, const void* idp) {
     std::memcpy(&id, idp, sizeof(id));
     BD_CUDA(cudaSetDevice(P.device));
     BD_NCCL(ncclCommInitRank(&P.comm, P.world, id, P.rank));
+}
+void pool_init_loopback(bd_pool* p, const char* group) {
+    PoolImpl& P = p->impl;
+    require(P.world > 1, BD_ERR_BAD_ARGUMENT, "init_loopback: pool was created with world_size 1");
+    require(P.comm == nullptr && P.loop == nullptr, BD_ERR_BAD_ARGUMENT,
+            "init_loopback: communicator already initialised");
+    std::shared_ptr<LoopbackGroup> g;
+    {
+        std::lock_guard<std::mutex> lk(g_loop_m);
+        auto& slot = g_loop_groups[group ? group : ""];
+        if (!slot || slot->world == 0) {
+            slot = std::make_shared<LoopbackGroup>();
+            slot->world = P.world;
+            slot->recv.assign(P.world, nullptr);
+            slot->ready.assign(P.world, nullptr);
+            slot->done.assign(P.world, nullptr);
+        }
+        require(slot->world == P.world, BD_ERR_BAD_ARGUMENT, "init_loopback: world size differs in group");
+        g = slot;
+    }
+    BD_CUDA(cudaSetDevice(P.device));
+    BD_CUDA(cudaEventCreateWithFlags(&P.lb_ready, cudaEventDisableTiming));
+    BD_CUDA(cudaEventCreateWithFlags(&P.lb_done, cudaEventDisableTiming));
+    P.loop = g;
+    P.use_graphs = false;  // the exchanges synchronise host threads: run eagerly
+    P.clear_plans();
 }
 void pool_stats(const bd_pool* p, bd_pool_stats* out) {
     *out = p->impl.stats;

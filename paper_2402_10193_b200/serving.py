@@ -69,6 +69,11 @@ class ServingPool:
         buf = C.create_string_buffer(uid, 128)
         check(lib().bd_pool_init_comm(self._h, buf))
 
+    def init_loopback(self, group: str) -> None:
+        """Test hook: the row-sharded pools of one process on one device exchange by device
+        copies instead of NCCL (drive each rank's decode from its own thread)."""
+        check(lib().bd_pool_init_loopback(self._h, group.encode()))
+
     # ---- backbone ----
     def set_tensor(self, name: str, data) -> None:
         import torch
