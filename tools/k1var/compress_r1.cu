@@ -14,8 +14,6 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
-#include <map>
-#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -25,19 +23,10 @@ namespace bd {
 namespace {
 
 constexpr int kThreads = 256;
-// 16-byte loads per tensor per thread per block, issued in groups of kLoadGroup (8 loads of
-// 16 B in flight per thread). Measured on B200 (tools/k1var, profiles/r02_exp_k1_vpt.txt,
-// algorithmic GB/s): bf16 Llama-2-70B layer set 4826 / 4232 / 5134 / 5390 at 4 / 8 / 16 / 32;
-// f32 4096^2 3244 / 4900 / 4290 / 4030 at 2 / 4 / 8 / 16.
-#ifndef BD_K1_VPT_BF16
-#define BD_K1_VPT_BF16 32
+#ifndef BD_K1_VPT
+#define BD_K1_VPT 4
 #endif
-#ifndef BD_K1_VPT_F32
-#define BD_K1_VPT_F32 4
-#endif
-template <bool kBf16>
-constexpr int kVecPerThread = kBf16 ? BD_K1_VPT_BF16 : BD_K1_VPT_F32;
-constexpr int kLoadGroup = 4;
+constexpr int kVecPerThread = BD_K1_VPT;  // 16-byte loads per tensor per thread per chunk
 constexpr int kMaxJobsPerLaunch = 192;
 
 struct Job {
@@ -104,7 +93,7 @@ template <bool kBf16>
 __global__ void __launch_bounds__(kThreads) compress_kernel(const __grid_constant__ JobTable tab) {
     using E = Elt<kBf16>;
     constexpr int P = E::kPerVec;              // elements per 16-byte vector
-    constexpr int kChunk = kThreads * kVecPerThread<kBf16> * P;  // elements per block
+    constexpr int kChunk = kThreads * kVecPerThread * P;  // elements per block
     __shared__ double s_red[kThreads / 32];
     __shared__ bool s_last;
 
@@ -124,8 +113,22 @@ __global__ void __launch_bounds__(kThreads) compress_kernel(const __grid_constan
 
     // warp-span layout: each iteration a warp covers 32*P consecutive elements
     // (lane l holds elements l*P .. l*P+P-1 of the span).
-    auto process = [&](int it, const float (&f)[P], const float (&b)[P]) {
+#pragma unroll
+    for (int it = 0; it < kVecPerThread; ++it) {
         const uint64_t span0 = blk * kChunk + (uint64_t(it) * (kThreads / 32) + warp) * 32 * P;
+        const uint64_t e0 = span0 + lane * P;
+        float f[P], b[P];
+        if (vec_ok && e0 + P <= n) {
+            E::load_vec(job.fine, e0, f);
+            if (job.base) E::load_vec(job.base, e0, b);
+        } else {
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                const bool in = e0 + k < n;
+                f[k] = in ? E::load(job.fine, e0 + k) : 0.0f;
+                b[k] = (in && job.base) ? E::load(job.base, e0 + k) : 0.0f;
+            }
+        }
         uint32_t mybits = 0;
 #pragma unroll
         for (int k = 0; k < P; ++k) {
@@ -141,36 +144,6 @@ __global__ void __launch_bounds__(kThreads) compress_kernel(const __grid_constan
         if (lane % kLanesPerWord == 0) {
             const uint64_t word_idx = span0 / 32 + lane / kLanesPerWord;
             if (word_idx * 32 < n) store_word(job.bits, word_idx, w, nbytes, bits_aligned);
-        }
-    };
-    auto e0_of = [&](int it) {
-        return blk * kChunk + (uint64_t(it) * (kThreads / 32) + warp) * 32 * P + lane * P;
-    };
-#pragma unroll 1
-    for (int it0 = 0; it0 < kVecPerThread<kBf16>; it0 += kLoadGroup) {
-        if (vec_ok && e0_of(it0 + kLoadGroup - 1) + P <= n) {
-            // fast path: all 2 x kLoadGroup 16-byte loads issued before any is consumed
-            float f[kLoadGroup][P], b[kLoadGroup][P];
-#pragma unroll
-            for (int g = 0; g < kLoadGroup; ++g) {
-                E::load_vec(job.fine, e0_of(it0 + g), f[g]);
-                if (job.base) E::load_vec(job.base, e0_of(it0 + g), b[g]);
-            }
-#pragma unroll
-            for (int g = 0; g < kLoadGroup; ++g) process(it0 + g, f[g], b[g]);
-        } else {
-#pragma unroll 1
-            for (int g = 0; g < kLoadGroup; ++g) {
-                const uint64_t e0 = e0_of(it0 + g);
-                float f[P], b[P];
-#pragma unroll
-                for (int k = 0; k < P; ++k) {
-                    const bool in = e0 + k < n;
-                    f[k] = in ? E::load(job.fine, e0 + k) : 0.0f;
-                    b[k] = (in && job.base) ? E::load(job.base, e0 + k) : 0.0f;
-                }
-                process(it0 + g, f, b);
-            }
         }
     }
 
@@ -228,34 +201,6 @@ __global__ void diff_kernel(float* res, const void* base, const void* fine, bool
     }
 }
 
-// Per-stream workspace (block partials + per-job arrival counters), grown on demand and
-// kept: the counters re-arm themselves at the end of every job (the last block resets its
-// counter), so a launch needs neither an allocation nor a memset. Concurrent launches on
-// one stream are ordered by the stream; different streams get different workspaces.
-struct Workspace {
-    char* ptr = nullptr;
-    size_t bytes = 0;
-};
-std::mutex g_ws_m;
-std::map<std::pair<int, cudaStream_t>, Workspace> g_ws;
-
-char* workspace(size_t need, cudaStream_t stream) {
-    int dev = 0;
-    BD_CUDA(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lk(g_ws_m);
-    Workspace& w = g_ws[{dev, stream}];
-    if (w.bytes < need) {
-        if (w.ptr) {
-            BD_CUDA(cudaStreamSynchronize(stream));  // earlier launches may still use it
-            BD_CUDA(cudaFree(w.ptr));
-        }
-        w.bytes = std::max(need, size_t(1) << 20);
-        BD_CUDA(cudaMalloc(reinterpret_cast<void**>(&w.ptr), w.bytes));
-        BD_CUDA(cudaMemsetAsync(w.ptr, 0, w.bytes, stream));  // counters start at 0
-    }
-    return w.ptr;
-}
-
 }  // namespace
 
 void note_launch();
@@ -265,7 +210,7 @@ void compress_launch(const bd_compress_job* jobs, int n_jobs, bd_dtype dtype,
     require(dtype == BD_F32 || dtype == BD_BF16, BD_ERR_UNSUPPORTED_DTYPE,
             "compress: dtype must be BD_F32 or BD_BF16");
     const bool bf16 = dtype == BD_BF16;
-    const uint64_t chunk = uint64_t(kThreads) * (bf16 ? kVecPerThread<true> * 8 : kVecPerThread<false> * 4);
+    const uint64_t chunk = uint64_t(kThreads) * kVecPerThread * (bf16 ? 8 : 4);
     for (int first = 0; first < n_jobs; first += kMaxJobsPerLaunch) {
         const int cnt = std::min(kMaxJobsPerLaunch, n_jobs - first);
         JobTable tab{};
@@ -287,16 +232,18 @@ void compress_launch(const bd_compress_job* jobs, int n_jobs, bd_dtype dtype,
             total_blocks += j.nblocks;
             total_partials += j.nblocks;
         }
-        // workspace: counters first (they stay zero between launches), then partials
-        char* ws = workspace(size_t(kMaxJobsPerLaunch) * sizeof(unsigned int) + 256 +
-                                 total_partials * sizeof(double), stream);
-        unsigned int* counters = reinterpret_cast<unsigned int*>(ws);
-        double* partials = reinterpret_cast<double*>(ws + size_t(kMaxJobsPerLaunch) * sizeof(unsigned int) + 256);
+        // workspace: partial sums + one counter per job (stream-ordered)
+        const size_t ws_bytes = total_partials * sizeof(double) + cnt * sizeof(unsigned int) + 16;
+        char* ws = nullptr;
+        BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), ws_bytes, stream));
+        BD_CUDA(cudaMemsetAsync(ws + total_partials * sizeof(double), 0,
+                                cnt * sizeof(unsigned int), stream));
         uint64_t off = 0;
         for (int i = 0; i < tab.n_jobs; ++i) {
-            tab.jobs[i].partial = partials + off;
+            tab.jobs[i].partial = reinterpret_cast<double*>(ws) + off;
             off += tab.jobs[i].nblocks;
-            tab.jobs[i].counter = counters + i;
+            tab.jobs[i].counter =
+                reinterpret_cast<unsigned int*>(ws + total_partials * sizeof(double)) + i;
         }
         if (bf16)
             compress_kernel<true><<<static_cast<unsigned>(total_blocks), kThreads, 0, stream>>>(tab);
@@ -304,6 +251,7 @@ void compress_launch(const bd_compress_job* jobs, int n_jobs, bd_dtype dtype,
             compress_kernel<false><<<static_cast<unsigned>(total_blocks), kThreads, 0, stream>>>(tab);
         note_launch();
         BD_CUDA(cudaGetLastError());
+        BD_CUDA(cudaFreeAsync(ws, stream));
     }
 }
 
