@@ -219,6 +219,8 @@ def run_ours(args, rank, world, dev):
     arch = dict(wl["arch"], rope_theta=10000.0)
     if args.layers:
         arch["n_layers"] = args.layers
+    if args.inter:  # shape experiments only (not a BASELINE config)
+        arch["intermediate"] = args.inter
     T = args.tenants or wl["tenants"]
     B = args.batch or wl["batch"]
     ctx = args.ctx or wl["ctx"]
@@ -288,17 +290,23 @@ def run_ours(args, rank, world, dev):
     prof = profile_step(pool, reqs(), x, y)
     for b in range(B):
         pos[b] += 1
+    # ---- serial profiled step: K2 and the delta kernel one after the other (the delta
+    # kernel's own HBM GB/s, the metric's second half) ----
+    prof_serial = profile_step(pool, reqs(), x, y, serial=True)
+    for b in range(B):
+        pos[b] += 1
 
     ms_step = ms_max / args.steps
     streams = 1 if tp else world  # independent batches in flight across the job
     tok_s = streams * B / (ms_step / 1e3)
     return dict(ms_step=ms_step, tok_s=tok_s, e2e_ms=e2e_ms, e2e_tok_s=streams * B / (e2e_ms / 1e3),
-                clocks=clk.summary(), kernels_per_step=kernels_per_step, prof=prof, arch=arch, T=T,
+                clocks=clk.summary(), kernels_per_step=kernels_per_step, prof=prof, prof_serial=prof_serial,
+                arch=arch, T=T,
                 B=B, ctx=ctx, setup_s=setup_s, launches=bd.launch_count() - launches0,
                 h2d=B * arch["dim"] * 4, d2h=B * arch["dim"] * 4)
 
 
-def profile_step(pool, reqs, x, y):
+def profile_step(pool, reqs, x, y, serial=False):
     import ctypes as C
 
     import torch
@@ -309,8 +317,8 @@ def profile_step(pool, reqs, x, y):
     arr = (Request * n)(*[Request(r, t, p) for r, t, p in reqs])
     ms = (C.c_double * len(PROF_KINDS))()
     cnt = (C.c_uint64 * len(PROF_KINDS))()
-    check(lib().bd_pool_profile_layers(pool._h, arr, n, x.data_ptr(), y.data_ptr(), ms, cnt,
-                                       torch.cuda.current_stream().cuda_stream))
+    fn = lib().bd_pool_profile_layers_serial if serial else lib().bd_pool_profile_layers
+    check(fn(pool._h, arr, n, x.data_ptr(), y.data_ptr(), ms, cnt, torch.cuda.current_stream().cuda_stream))
     return {k: {"ms": ms[i], "count": cnt[i]} for i, k in enumerate(PROF_KINDS)}
 
 
@@ -484,6 +492,32 @@ def cpu_reference_compress(budget_matrices=None):
                       f"({secs.value:.2f} s)"}
 
 
+def delta_kernel(res, hbm_peak, peak_kind):
+    """The tenant-delta kernel on its own (serial profile: K2 and K3 one after the other):
+    algorithmic bytes (every tenant plane once + activations + f32 partials) per launch /
+    its average launch time, per projection group and for the dominant group."""
+    arch, T, B = res["arch"], res["T"], res["B"]
+    d, kv, inter = arch["dim"], arch["kv_dim"], arch["intermediate"]
+    shapes = {"qkv": (d + 2 * kv, d), "o": (d, d), "gu": (2 * inter, d), "down": (d, inter)}
+    prof = res["prof_serial"]
+    groups = {}
+    for g, (rows, cols) in shapes.items():
+        k = prof.get(f"delta_{g}")
+        if not k or not k["count"]:
+            continue
+        slices = -(-cols // 1024)
+        algo = T * rows * cols / 8 + 2 * B * cols + 4 * B * rows * slices
+        ms = k["ms"] / k["count"]
+        groups[g] = {"gbs": round(algo / (ms / 1e3) / 1e9, 1), "avg_launch_ms": round(ms, 5),
+                     "algorithmic_bytes_per_launch": algo}
+    if not groups:  # K23 (base and deltas in one kernel): no separate delta kernel
+        return {"kernel": "fused (K23)", "note": "deltas run inside the base GEMM kernel"}
+    dom = max(groups, key=lambda g: groups[g]["avg_launch_ms"])
+    return {"kernel": f"delta_{dom}", "bound": "hbm", "achieved": groups[dom]["gbs"], "peak": hbm_peak,
+            "peak_kind": peak_kind, "unit": "GB/s", "frac": round(groups[dom]["gbs"] / hbm_peak, 4),
+            "per_group": groups, "how": "serial profiled step (K2 then K3), CUDA events on the launch stream"}
+
+
 # ------------------------------------------------------------------ cpu arm --
 def cpu_reference_tok_s(arch, T, B, budget_s=12.0):
     """Reference deltakit (oracle/_ref) on a bounded sample: the per-projection work
@@ -611,6 +645,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="l7_stack", choices=sorted(WORKLOADS) + sorted(COMPRESS))
     ap.add_argument("--layers", type=int, default=0, help="override the workload's layer count")
+    ap.add_argument("--inter", type=int, default=0, help="override the FFN width (shape experiments)")
     ap.add_argument("--tenants", type=int, default=0)
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--ctx", type=int, default=0, help="context length before timing (default: workload)")
@@ -673,6 +708,7 @@ def main():
                     "d2h_bytes_per_step": res["d2h"]},
             "gpu_launches": res["kernels_per_step"] * args.steps,
             "roofline": rl,
+            "delta_kernel": delta_kernel(res, hbm, kind),
             "step_roofline": {"algorithmic_bytes": byts["base"] + byts["bits"],
                               "kv_bytes": kv_bytes(res["arch"], res["B"], res["ctx"]),
                               "achieved_gbs": round((byts["base"] + byts["bits"]) / (res["ms_step"] / 1e3) / 1e9, 1),

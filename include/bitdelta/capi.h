@@ -221,6 +221,10 @@ enum bd_prof_kind {
 };
 int bd_pool_profile_layers(bd_pool* pool, const bd_request* reqs, uint64_t n, const float* x_in,
                            float* x_out, double* ms_out, uint64_t* count_out, void* stream);
+/* Same, with the base GEMM (K2) and the tenant-delta kernel (K3) run one after the other
+ * instead of side by side, so each is timed on its own (the delta kernel's own GB/s). */
+int bd_pool_profile_layers_serial(bd_pool* pool, const bd_request* reqs, uint64_t n, const float* x_in,
+                                  float* x_out, double* ms_out, uint64_t* count_out, void* stream);
 
 typedef struct bd_pool_stats {
     uint64_t backbone_passes; /* serve.hpp:77 */

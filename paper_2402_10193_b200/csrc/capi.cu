@@ -75,7 +75,7 @@ void pool_decode_layers(bd_pool* p, const bd_request* r, uint64_t n, const float
                         void* s);
 void pool_stats(const bd_pool* p, bd_pool_stats* out);
 void pool_profile_layers(bd_pool* p, const bd_request* r, uint64_t n, const float* xin,
-                         float* xout, double* ms, uint64_t* cnt, void* s);
+                         float* xout, double* ms, uint64_t* cnt, void* s, bool serial);
 void nccl_unique_id(void* out);
 void pool_init_comm(bd_pool* p, const void* id);
 void pool_init_loopback(bd_pool* p, const char* group);
@@ -129,15 +129,15 @@ void multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int32_
     }
     static const char* mode_env = std::getenv("BD_DELTA");
     const std::string mode = mode_env ? mode_env : "auto";
-    size_t max_per_tenant = 0;
-    for (int t : order) max_per_tenant = std::max(max_per_tenant, by_t[t].size());
+    size_t with_delta = 0;
+    for (int t : order) with_delta += by_t[t].size();
+    const double mean_per_tenant = order.empty() ? 0.0 : double(with_delta) / double(order.size());
     // ---- K23: base GEMM + FP4 tensor-core deltas in one persistent kernel ----
     bool aligned16 = in_dim % 128 == 0 && out_dim % 128 == 0;
     for (int t : order) aligned16 &= (reinterpret_cast<uintptr_t>(tenant_bits[t]) % 16) == 0;
-    // K23 from 4 requests per tenant (its plane is then read once per slot of 4 requests
-    // instead of once per request): Mistral-7B sweep at batch 64, 4 requests/tenant +30 %
-    // over the byte LUT (k23_min_requests)
-    if ((mode == "mt4" || (mode == "auto" && int(max_per_tenant) >= k23_min_requests(batch))) && aligned16 &&
+    // K23 when tenants average k23_min_requests(batch) requests or more (a plane is then read
+    // once per slot of up to 4 requests instead of once per request; same policy as the pool)
+    if ((mode == "mt4" || (mode == "auto" && mean_per_tenant >= k23_min_requests(batch))) && aligned16 &&
         !order.empty() && batch <= 64) {
         Mt4Params prm{};
         prm.n_subs = 1;
@@ -187,141 +187,49 @@ void multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int32_
             prm.bits_maps = dmaps;
             prm.partial = P;
             xp_prep_launch(X, int(in_dim), int(in_dim), batch, xpk, stream);
-            static const bool tr = std::getenv("BD_MT4_TRACE") != nullptr;
-            if (tr) {
-                BD_CUDA(cudaMalloc(&prm.trace, 8 * 512 * sizeof(long long)));
-                BD_CUDA(cudaMemset(prm.trace, 0, 8 * 512 * sizeof(long long)));
-                mt4_launch(prm, stream);  // warm
-            }
             mt4_launch(prm, stream);
-            if (tr) {
-                std::vector<long long> h(8 * 512);
-                BD_CUDA(cudaMemcpyAsync(h.data(), prm.trace, h.size() * 8, cudaMemcpyDeviceToHost, stream));
-                BD_CUDA(cudaStreamSynchronize(stream));
-                const long long t0 = h[512];
-                fprintf(stderr, "stage: clock64 of the trace points (role 0..7) relative to the MMA warp's first full\n");
-                for (int i = 0; i < 512; ++i) {
-                    if (!h[512 + i]) break;
-                    fprintf(stderr, "%4d", i);
-                    for (int r = 0; r < 8; ++r) fprintf(stderr, " %8lld", h[r * 512 + i] ? h[r * 512 + i] - t0 : -1);
-                    fprintf(stderr, "\n");
-                }
-                BD_CUDA(cudaFree(prm.trace));
-                prm.trace = nullptr;
-            }
             combine_launch(P, prm.splits, nullptr, batch, int(out_dim), Y, stream);
             BD_CUDA(cudaFreeAsync(ws, stream));
             return;
         }
     }
     // ---- byte-LUT path (few requests per tenant): tcgen05 base GEMM + K3 LUT ----
-    if ((mode == "lut" || mode == "auto") && !order.empty() &&
-        batch <= kLutMaxJobs) {
-        LutParams prm{};
-        for (int b = 0; b < batch; ++b) {
-            const int t = req_tenant ? req_tenant[b] : -1;
-            if (t < 0) continue;
-            LutJob& j = prm.jobs[prm.n_jobs++];
-            j.req = b;
-            j.n_planes[0] = 1;
-            j.bits[0][0] = tenant_bits[t];
-            j.alpha[0][0] = tenant_alpha[t];
-        }
+    // one launch per kLutMaxJobs requests; each writes its own requests' rows of D
+    if ((mode == "lut" || mode == "auto") && !order.empty()) {
+        std::vector<LutParams> prms;
+        bool ok = true;
         const int seg_rows[1] = {int(out_dim)};
-        if (plan_lut(prm, seg_rows, 1, int(in_dim), int(in_dim), batch)) {
+        int n_jobs = 0;
+        for (int b0 = 0; b0 < batch && ok; b0 += kLutMaxJobs) {
+            LutParams prm{};
+            for (int b = b0; b < std::min(batch, b0 + kLutMaxJobs); ++b) {
+                const int t = req_tenant ? req_tenant[b] : -1;
+                if (t < 0) continue;
+                LutJob& j = prm.jobs[prm.n_jobs++];
+                j.req = b;
+                j.n_planes[0] = 1;
+                j.bits[0][0] = tenant_bits[t];
+                j.alpha[0][0] = tenant_alpha[t];
+            }
+            n_jobs += prm.n_jobs;
+            if (prm.n_jobs == 0) continue;
+            ok = plan_lut(prm, seg_rows, 1, int(in_dim), int(in_dim), batch);
+            prms.push_back(prm);
+        }
+        if (ok && !prms.empty()) {
+            const int slices = prms[0].slices;
             float* P = nullptr;
             float* D = nullptr;
             BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&P), sizeof(float) * g.splits * batch * out_dim, stream));
-            BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&D), sizeof(float) * prm.slices * batch * out_dim, stream));
+            BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&D), sizeof(float) * slices * batch * out_dim, stream));
             // base-only requests have no job: their delta slices must read as zero
-            if (size_t(prm.n_jobs) < size_t(batch))
-                BD_CUDA(cudaMemsetAsync(D, 0, sizeof(float) * prm.slices * batch * out_dim, stream));
+            if (n_jobs < batch)
+                BD_CUDA(cudaMemsetAsync(D, 0, sizeof(float) * slices * batch * out_dim, stream));
             base_gemm_launch(g, mw, mx, P, stream);
-            lut_launch(prm, X, D, stream);
-            combine_launch(P, g.splits, D, batch, int(out_dim), Y, stream, prm.slices);
+            for (const LutParams& prm : prms) lut_launch(prm, X, D, stream);
+            combine_launch(P, g.splits, D, batch, int(out_dim), Y, stream, slices);
             BD_CUDA(cudaFreeAsync(P, stream));
             BD_CUDA(cudaFreeAsync(D, stream));
-            return;
-        }
-    }
-    // ---- fused tensor-core path (K2+K3 in one kernel) when eligible ----
-    static const bool no_fused = (std::getenv("BD_NO_FUSED") && std::getenv("BD_NO_FUSED")[0] != '0') ||
-                                 mode == "units";
-    bool aligned = in_dim % 128 == 0;
-    for (int t : order) aligned &= (reinterpret_cast<uintptr_t>(tenant_bits[t]) % 16) == 0;
-    if (!no_fused && aligned && !order.empty()) {
-        FusedParams prm{};
-        prm.n_subs = 1;
-        prm.sub_row0[0] = 0;
-        prm.sub_row0[1] = int(out_dim);
-        std::vector<int> xq_row(batch, 0);
-        std::vector<CUtensorMap> maps;
-        std::vector<const uint8_t*> map_ptrs;
-        int rows = 0, slot = 0;
-        bool ok = true;
-        for (int t : order) {
-            const auto& rq = by_t[t];
-            for (size_t c = 0; c < rq.size(); c += kFusedMaxReq) {
-                if (slot >= kFusedMaxSlots) { ok = false; break; }
-                FusedSlot& fs = prm.slots[slot++];
-                fs.n_req = int(std::min<size_t>(kFusedMaxReq, rq.size() - c));
-                fs.xrow = rows;
-                for (int q = 0; q < fs.n_req; ++q) {
-                    fs.req[q] = rq[c + q];
-                    xq_row[rq[c + q]] = rows + 2 * q;
-                }
-                rows += ((std::max(2 * fs.n_req, 8) + 7) / 8) * 8;
-                fs.alpha[0] = tenant_alpha[t];
-                int mi = -1;  // one descriptor per distinct plane pointer
-                for (int j = 0; j < slot - 1 && mi < 0; ++j)
-                    if (tenant_bits[order[0]] && prm.slots[j].map_idx[0] >= 0 &&
-                        map_ptrs[prm.slots[j].map_idx[0]] == tenant_bits[t])
-                        mi = prm.slots[j].map_idx[0];
-                if (mi < 0) {
-                    mi = int(maps.size());
-                    maps.push_back(tmap_bits(tenant_bits[t], out_dim, in_dim));
-                    map_ptrs.push_back(tenant_bits[t]);
-                }
-                fs.map_idx[0] = mi;
-            }
-        }
-        prm.n_slots = slot;
-        if (ok && plan_fused(prm, out_dim, in_dim, batch)) {
-            const uint64_t kpad = uint64_t(prm.kb_total) * kFusedBK;
-            char* ws = nullptr;
-            const size_t sz_p = sizeof(float) * prm.splits * batch * out_dim;
-            // base-only requests get scratch rows past the slots' TMA box
-            for (int b = 0; b < batch; ++b)
-                if (req_tenant == nullptr || req_tenant[b] < 0) xq_row[b] = prm.xq_rows + 2 * b;
-            const size_t sz_q = size_t(prm.xq_rows + 2 * batch) * kpad;
-            const size_t sz_m = maps.size() * sizeof(CUtensorMap);
-            const size_t sz_s = sizeof(int) * batch * 2 * (prm.kb_total + 1);
-            const size_t total = sz_p + sz_q + sz_m + sz_s + sizeof(float) * batch + sizeof(int) * batch + 512;
-            BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), total, stream));
-            char* cur = ws;
-            auto take = [&](size_t n) { char* r = cur; cur += (n + 127) & ~size_t(127); return r; };
-            float* P = reinterpret_cast<float*>(take(sz_p));
-            int8_t* Xq = reinterpret_cast<int8_t*>(take(sz_q));
-            CUtensorMap* dmaps = reinterpret_cast<CUtensorMap*>(take(sz_m));
-            int* qsum = reinterpret_cast<int*>(take(sz_s));
-            float* xscale = reinterpret_cast<float*>(take(sizeof(float) * batch));
-            int* dxr = reinterpret_cast<int*>(take(sizeof(int) * batch));
-            BD_CUDA(cudaMemsetAsync(Xq, 0, sz_q, stream));
-            BD_CUDA(cudaMemcpyAsync(dmaps, maps.data(), sz_m, cudaMemcpyHostToDevice, stream));
-            BD_CUDA(cudaMemcpyAsync(dxr, xq_row.data(), sizeof(int) * batch, cudaMemcpyHostToDevice, stream));
-            BD_CUDA(cudaStreamSynchronize(stream));  // host staging (maps, rows) consumed
-            prm.map_w = mw;
-            prm.map_x = mx;
-            prm.map_xq = tmap_xq(Xq, prm.xq_rows, kpad, kpad);
-            prm.bits_maps = dmaps;
-            prm.xscale = xscale;
-            prm.qsum = qsum;
-            prm.partial = P;
-            xq_prep_launch(X, int(in_dim), int(in_dim), batch, dxr, Xq, int(kpad), xscale, qsum,
-                           prm.kb_total, stream);
-            fused_launch(prm, stream);
-            combine_launch(P, prm.splits, nullptr, batch, int(out_dim), Y, stream);
-            BD_CUDA(cudaFreeAsync(ws, stream));
             return;
         }
     }
@@ -563,7 +471,14 @@ int bd_pool_profile_layers(bd_pool* pool, const bd_request* reqs, uint64_t n, co
                            float* x_out, double* ms_out, uint64_t* count_out, void* stream) {
     return guarded([&] {
         require(pool != nullptr, BD_ERR_BAD_ARGUMENT, "null pool");
-        pool_profile_layers(pool, reqs, n, x_in, x_out, ms_out, count_out, stream);
+        pool_profile_layers(pool, reqs, n, x_in, x_out, ms_out, count_out, stream, false);
+    });
+}
+int bd_pool_profile_layers_serial(bd_pool* pool, const bd_request* reqs, uint64_t n, const float* x_in,
+                                  float* x_out, double* ms_out, uint64_t* count_out, void* stream) {
+    return guarded([&] {
+        require(pool != nullptr, BD_ERR_BAD_ARGUMENT, "null pool");
+        pool_profile_layers(pool, reqs, n, x_in, x_out, ms_out, count_out, stream, true);
     });
 }
 int bd_pool_get_stats(const bd_pool* pool, bd_pool_stats* out) {

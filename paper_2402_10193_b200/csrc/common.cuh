@@ -319,21 +319,25 @@ __device__ __forceinline__ void bulk_load_w(void* smem_dst, const void* src, uin
 // (griddepcontrol.wait: the predecessor grid has completed and its writes are
 // visible) before touching anything the predecessor produced. A no-op when the
 // kernel was launched without the attribute.
+// CTA-scope acquire load / release store (generic address: shared or global)
+__device__ __forceinline__ uint32_t ld_acquire_cta(const volatile uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.cta.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_cta(volatile uint32_t* p, uint32_t v) {
+    asm volatile("st.release.cta.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 // Allow the dependent (PDL-launched) grid to be scheduled now: its CTAs start their
 // predecessor-independent prologue (constant plane/weight loads) while this grid runs;
 // they still block in griddep_wait() until this grid has completed.
-#ifndef BD_LINEAR_TRIGGER
-#define BD_LINEAR_TRIGGER 0  // 1: K2 / K3 let the next glue kernel be scheduled at entry (measured: glue CTAs parked beside the linears slow them)
-#endif
 __device__ __forceinline__ void griddep_launch_dependents() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-inline bool pdl_enabled() {
-    static const bool on = !(std::getenv("BD_PDL") && std::getenv("BD_PDL")[0] == '0');
-    return on;
-}
+inline bool pdl_enabled() { return true; }
 // kernels launched through launch_pdl() wait (griddep_wait) before consuming their
 // predecessors' outputs, so a captured graph may give them programmatic in-edges
 void note_pdl_kernel(const void* fn);

@@ -91,7 +91,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t taddr = *tmem_slot;
-    if (BD_LINEAR_TRIGGER) griddep_launch_dependents();  // the next glue kernel may be scheduled
 
     if (warp == 0 && lane == 0) {
         // ---- TMA producer ----

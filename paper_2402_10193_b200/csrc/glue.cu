@@ -235,49 +235,6 @@ __global__ void __launch_bounds__(kRnThreads)
     if (threadIdx.x == 0) trace_rec(TR_NORM, t_entry, t_wait);
 }
 
-// single-kernel variant: one 1024-thread block per request does the residual add,
-// the double sum of squares (fixed tree) and the normalisation
-constexpr int kFusedNormThreads = 1024;
-__global__ void __launch_bounds__(kFusedNormThreads)
-    resid_norm_one_kernel(float* __restrict__ x, int dim, ProjOut proj, const float* const* __restrict__ norm_w,
-                          uint16_t* __restrict__ xn, int ldxn, float* __restrict__ xn_f32) {
-    __shared__ double red_d[32];
-    const int b = blockIdx.x;
-    float* xb = x + size_t(b) * dim;
-    constexpr int kMaxPer = 16;
-    float v[kMaxPer];
-    double sq = 0.0;
-#pragma unroll
-    for (int k = 0; k < kMaxPer; ++k) {
-        const int i = threadIdx.x + k * kFusedNormThreads;
-        if (i < dim) {
-            float t = xb[i];
-            if (proj.P || proj.G) t = t + proj_val(proj, b, proj.col0 + i);
-            v[k] = t;
-            sq += static_cast<double>(t) * t;
-        }
-    }
-    if (proj.P || proj.G)
-#pragma unroll
-        for (int k = 0; k < kMaxPer; ++k) {
-            const int i = threadIdx.x + k * kFusedNormThreads;
-            if (i < dim) xb[i] = v[k];
-        }
-    if (!norm_w) return;
-    sq = block_sum(sq, red_d);
-    const double inv = 1.0 / sqrt(sq / static_cast<double>(dim) + 1e-12);
-    const float* w = norm_w[b];
-#pragma unroll
-    for (int k = 0; k < kMaxPer; ++k) {
-        const int i = threadIdx.x + k * kFusedNormThreads;
-        if (i < dim) {
-            const float y = static_cast<float>(static_cast<double>(v[k]) * inv) * w[i];
-            if (xn) xn[size_t(b) * ldxn + i] = f32_to_bf16(y);
-            if (xn_f32) xn_f32[size_t(b) * dim + i] = y;
-        }
-    }
-}
-
 // one block per (head, request): RoPE, KV append, scores, softmax, context
 __global__ void attn_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos_dev,
                             uint16_t* __restrict__ ctx_out, int ld_ctx) {
@@ -748,8 +705,7 @@ void resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const 
     // one-launch path: the CTAs of a request meet on an arrival counter, so the whole
     // grid must be co-resident (<= 8 CTAs per SM here) -> bounded grid size
     const int nc = (dim + kRnChunk - 1) / kRnChunk;
-    static const bool two_phase = std::getenv("BD_NORM_TWO") && std::getenv("BD_NORM_TWO")[0] == '1';
-    if (!two_phase && dim % 4 == 0 && ldxn % 4 == 0 && proj_vec4_ok(proj) &&
+    if (dim % 4 == 0 && ldxn % 4 == 0 && proj_vec4_ok(proj) &&
         size_t(nc) * batch <= size_t(kNumSMs) * 8) {
         BD_CUDA(launch_pdl(resid_norm_kernel, dim3(nc, batch), dim3(kRnThreads), 0, s, x, dim, proj, norm_w, xn,
                            ldxn, xn_f32, arrive, msq_ws));
@@ -757,15 +713,7 @@ void resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const 
         BD_CUDA(cudaGetLastError());
         return;
     }
-    // One-launch variant (16 CTAs) measured slower than the two-phase, 16x wider
-    // grid at batch 16 (1.22 vs 0.73 ms/step); kept for BD_NORM_ONE=1 experiments.
-    static const bool one = std::getenv("BD_NORM_ONE") && std::getenv("BD_NORM_ONE")[0] == '1';
-    if (one && dim <= 16 * kFusedNormThreads) {
-        resid_norm_one_kernel<<<batch, kFusedNormThreads, 0, s>>>(x, dim, proj, norm_w, xn, ldxn, xn_f32);
-        note_launch();
-        BD_CUDA(cudaGetLastError());
-        return;
-    }
+    // two-phase fallback (unaligned shapes / grids too wide to be co-resident)
     const dim3 grid(norm_chunks(dim), batch);
     resid_kernel<<<grid, kNormChunk, 0, s>>>(x, dim, proj, norm_w ? msq_ws : nullptr);
     note_launch();
@@ -778,8 +726,7 @@ void resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const 
 
 void attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int batch,
                  uint16_t* ctx, int ld_ctx, cudaStream_t s) {
-    static const bool old = std::getenv("BD_ATTN_OLD") && std::getenv("BD_ATTN_OLD")[0] == '1';
-    if (!old && a.hd == 128 && a.kv_dim % 8 == 0 && a.dim % 8 == 0) {
+    if (a.hd == 128 && a.kv_dim % 8 == 0 && a.dim % 8 == 0) {
         // one staging buffer of up to 192 rows (48 KB: K, then V): four CTAs per SM,
         // so batch x heads = 512 CTAs run as a single wave on 148 SMs
         const int rows = std::min(192, std::max(32, a.max_seq));

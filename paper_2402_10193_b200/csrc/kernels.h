@@ -58,47 +58,6 @@ struct DeltaUnit {
 void delta_units_launch(const DeltaUnit* units_host, int n_units, const void* X, int ldx,
                         int cols, int batch, float* D, int out_rows, cudaStream_t stream);
 
-// ---- K2+K3 fused: base GEMM + tenant deltas on the tensor cores ----
-// The sign planes are expanded in registers to u8 {0,128} A tiles written to
-// TMEM and multiplied (tcgen05.mma kind::i8) with the activations quantised
-// to two int8 fixed-point pieces; see mtfused.cu for the numerics.
-constexpr int kFusedMaxSlots = 32;
-constexpr int kFusedMaxSubs = 3;
-constexpr int kFusedMaxReq = 32;
-struct FusedSlot {
-    int dcol;                    // TMEM column of this slot's s32 accumulator
-    int n;                       // MMA N (8 or a multiple of 16)
-    int xrow;                    // first Xq row (multiple of 8)
-    int n_req;
-    int req[kFusedMaxReq];       // batch indices, pieces at rows xrow + 2q, 2q+1
-    float alpha[kFusedMaxSubs];  // per stacked sub-matrix
-    int map_idx[kFusedMaxSubs];  // index into the bits tensor-map table
-};
-struct FusedParams {
-    CUtensorMap map_w, map_x, map_xq;
-    const CUtensorMap* bits_maps;  // device table
-    const float* xscale;           // [batch] fixed-point scale per request
-    const int* qsum;               // [batch][2][kb_total+1] prefix sums of the pieces
-    float* partial;                // [splits][batch][M]
-    int M, batch, bn, kb_total, kb_per_split, splits, m_tiles, stages, smem;
-    int n_slots, n_subs;
-    int sub_row0[kFusedMaxSubs + 1];
-    int a_col0, tmem_cols, xq_rows;
-    int ring;   // TMEM A-operand ring entries (32 columns each)
-    int debug;  // experiment flags (0 in production)
-    FusedSlot slots[kFusedMaxSlots];
-};
-constexpr int kFusedBK = 128;
-// Fills the tiling fields (bn, stages, splits, TMEM layout) given slots; false if it does not fit.
-bool plan_fused(FusedParams& p, uint64_t M, uint64_t K, int batch);
-void fused_launch(const FusedParams& p, cudaStream_t stream);
-// X bf16 [batch x ldx] -> Xq int8 [xq_rows x ldq] (permuted K, 2 pieces per request at
-// rows xq_row[b], +1), xscale[b], qsum[b][2][kb+1]
-void xq_prep_launch(const void* X, int ldx, int K, int batch, const int* xq_row_dev, int8_t* Xq,
-                    int ldq, float* xscale, int* qsum, int kb_total, cudaStream_t stream);
-CUtensorMap tmap_bits(const uint8_t* bits, uint64_t rows, uint64_t cols);
-CUtensorMap tmap_xq(const int8_t* Xq, int rows, uint64_t K, uint64_t ldq);
-
 // ---- K23: base GEMM + tenant deltas as FP4 (kind::mxf4) MMAs in one persistent kernel (mt4.cu) ----
 constexpr int kMt4MaxSlots = 64;
 constexpr int kMt4MaxReq = 4;   // requests per slot (MMA N = 8 pieces x n_req <= 32)
@@ -120,18 +79,12 @@ struct Mt4Params {
     int sub_row0[kMt4MaxSubs + 1];
     int kb_base, kc_plane, stages_per_tile, grid, splits, ring_b, ring_p, smem, n_chunks;
     int col_base, col_acc, acc_stride, n_acc, col_sfa, col_ring, n_ring;  // TMEM layout
-    int debug;  // experiment flags (BD_MT4_DEBUG), 0 in production
-    long long* trace;  // CTA 0 clock64 timeline (BD_MT4_TRACE), null in production
     Mt4Slot slots[kMt4MaxSlots];
 };
-// requests per tenant from which the auto policy uses K23 (BD_K23_MIN_REQ overrides): 4, or 2
-// at batch >= 64. Measured at 2 requests/tenant (K23 vs byte LUT): Mistral-7B B=64 +8 %,
-// Llama-2-7B B=64 +3 %, Mistral-7B B=32 +1 %, Llama-2-7B B=32 -2 %, Llama-2-7B B=16 -22 %.
-inline int k23_min_requests(int batch = 0) {
-    static const int v = std::getenv("BD_K23_MIN_REQ") ? std::atoi(std::getenv("BD_K23_MIN_REQ")) : 0;
-    if (v > 0) return v;
-    return batch >= 64 ? 2 : 4;
-}
+// mean requests per tenant from which the auto policy uses K23: 4, or 2 at batch >= 64.
+// Measured at 2 requests/tenant (K23 vs byte LUT): Mistral-7B B=64 +8 %, Llama-2-7B B=64
+// +3 %, Mistral-7B B=32 +1 %, Llama-2-7B B=32 -2 %, Llama-2-7B B=16 -22 %.
+inline int k23_min_requests(int batch = 0) { return batch >= 64 ? 2 : 4; }
 // requests in the next K23 slot of a tenant with `remaining` requests left (slots of 4, then
 // the remainder)
 inline int mt4_slot_requests(size_t remaining) {
@@ -163,7 +116,6 @@ struct LutJob {
 };
 struct LutParams {
     int n_jobs, slices, cols, ldx, batch, M, n_segs, grid;
-    int debug;  // experiment flags (BD_LUT_DEBUG), 0 in production
     int seg_row0[kLutMaxSegs + 1];  // stacked row offsets of the sub-matrices
     LutJob jobs[kLutMaxJobs];
 };
@@ -171,29 +123,6 @@ struct LutParams {
 bool plan_lut(LutParams& p, const int* seg_rows, int n_segs, int cols, int ldx, int batch);
 // out: [slices][batch][M] f32, alpha already applied; every (slice, req, row) of a job written
 void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream);
-// K3b (bmma.cu): same plan and output as the LUT on the binary tensor-core path
-// (cols % 128 == 0, 16-byte aligned planes; BD_LUT_B1=0 disables)
-bool b1_supported(const LutParams& p);
-void b1_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream);
-
-// ---- K3t: tenant deltas alone on the FP4 tensor cores, beside K2 (mxd.cu) ----
-// Same work and output as the LUT plan (D[slice][batch][M], alpha applied); one sign
-// plane per (job, segment), segment rows % 128 == 0, activations as FP4 pieces (xp_prep).
-struct MxdJob {
-    int req;
-    float alpha[kLutMaxSegs];
-};
-struct MxdParams {
-    const CUtensorMap* maps;  // device table [n_jobs * n_segs] (tmap_bits4)
-    const uint8_t* xpk;       // [batch][n_chunks][kXpBlock]
-    long long total_stages;
-    int n_jobs, n_segs, M, m_tiles, cols, batch, slices, n_chunks, grid, smem;
-    int seg_row0[kLutMaxSegs + 1];
-    MxdJob jobs[kLutMaxJobs];
-};
-// Fills the geometry from n_jobs/jobs and the segment rows; false if unsupported (BD_MXD=0 disables).
-bool plan_mxd(MxdParams& p, const int* seg_rows, int n_segs, int cols, int batch);
-void mxd_launch(const MxdParams& p, float* out, cudaStream_t stream);
 
 // ---- K5: fp32 multi-tenant linear (SIMT, fp64 accumulation; packed.cu) ----
 // Y[b] = W x_b + alpha_b S_b x_b for every b < batch (req_bits[b] == null: base only);

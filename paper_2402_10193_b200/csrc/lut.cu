@@ -82,7 +82,6 @@ __global__ void __maxnreg__(kLutRegs)
     extern __shared__ float T[];
     __shared__ float xs[32 * 33];  // x of the slice, [lane][32 columns] padded to 33
     const unsigned long long t_entry = gtimer();
-    if (BD_LINEAR_TRIGGER) griddep_launch_dependents();  // the next glue kernel may be scheduled
     griddep_wait();  // PDL: X comes from the previous kernel; D is still read by it
     const unsigned long long t_wait = gtimer();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -110,7 +109,7 @@ __global__ void __maxnreg__(kLutRegs)
             for (int i = threadIdx.x; i < kSliceCols; i += kLutThreads)
                 xs[(i >> 5) * 33 + (i & 31)] = (c0 + i < p.cols) ? bf16_to_f32(xr[c0 + i]) : 0.0f;
             __syncthreads();
-            if (!(p.debug & 1) && threadIdx.x < 512) build_tables(T, xs);  // 512 builders: 128 tables x 4 quarters
+            if (threadIdx.x < 512) build_tables(T, xs);  // 512 builders: 128 tables x 4 quarters
             __syncthreads();
             cur = u;
         }
@@ -382,7 +381,6 @@ bool plan_lut(LutParams& p, const int* seg_rows, int n_segs, int cols, int ldx, 
     // persistent: one CTA per SM, but keep >= 512 rows of work per CTA
     const long long work = static_cast<long long>(p.n_jobs) * p.slices * p.M;
     p.grid = static_cast<int>(std::max<long long>(1, std::min<long long>(kNumSMs, work / 512)));
-    p.debug = std::getenv("BD_LUT_DEBUG") ? std::atoi(std::getenv("BD_LUT_DEBUG")) : 0;
     return true;
 }
 
@@ -396,13 +394,9 @@ void lut_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t st
         // helps when plane rows are 128-B aligned (qkv/o/gu: -0.34 ms/step) and hurts
         // the down projection (1376-B rows, every warp load spans two lines: +0.35 ms),
         // where the default carveout keeps the two kernels on mostly disjoint SMs.
-        static const bool carve_all = std::getenv("BD_LUT_CARVE_ALL") && std::getenv("BD_LUT_CARVE_ALL")[0] == '1';
-        static const int carve_un = std::getenv("BD_LUT_CARVE_UN") ? std::atoi(std::getenv("BD_LUT_CARVE_UN")) : -1;
-        if ((kWPR % 32 == 0 && kWPR > 0) || carve_all)
+        if (kWPR % 32 == 0 && kWPR > 0)
             BD_CUDA(cudaFuncSetAttribute(lut_kernel<kWPR>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          int(cudaSharedmemCarveoutMaxShared)));
-        else if (carve_un >= 0)
-            BD_CUDA(cudaFuncSetAttribute(lut_kernel<kWPR>, cudaFuncAttributePreferredSharedMemoryCarveout, carve_un));
         attr = true;
     }
     BD_CUDA(launch_pdl(lut_kernel<kWPR>, dim3(p.grid), dim3(kLutThreads), kTableBytes, stream, p,
@@ -416,11 +410,11 @@ void lut2_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t s
         BD_CUDA(cudaFuncSetAttribute(lut2_kernel<kWPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(kTableBytes)));
         // max carveout (K2 co-resident on every SM) where plane rows are 128-B aligned; the
-        // down projection (1376-B rows) measured faster on the default carveout (as v1)
-        static const int carve = std::getenv("BD_LUT2_CARVE") ? std::atoi(std::getenv("BD_LUT2_CARVE")) : -2;
-        if (carve >= 0 || (carve == -2 && kWPR % 32 == 0 && kWPR > 0))
+        // down projection (1376-B rows) measured faster on the default carveout, K2 after
+        // it (profiles/r02_exp_down_carveout.txt: 1.487 vs 1.857 ms/step for down)
+        if (kWPR % 32 == 0 && kWPR > 0)
             BD_CUDA(cudaFuncSetAttribute(lut2_kernel<kWPR>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                         carve >= 0 ? carve : int(cudaSharedmemCarveoutMaxShared)));
+                                         int(cudaSharedmemCarveoutMaxShared)));
         attr = true;
     }
     BD_CUDA(launch_pdl(lut2_kernel<kWPR>, dim3(p.grid), dim3(kLutThreads), kTableBytes, stream, p,
@@ -428,8 +422,7 @@ void lut2_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t s
 }
 
 static bool lut2_ok(const LutParams& p) {
-    static const bool v1 = std::getenv("BD_LUT_V1") && std::getenv("BD_LUT_V1")[0] == '1';
-    if (v1 || p.cols % 128 != 0) return false;
+    if (p.cols % 128 != 0) return false;
     for (int j = 0; j < p.n_jobs; ++j)
         for (int s = 0; s < p.n_segs; ++s)
             for (int k = 0; k < p.jobs[j].n_planes[s]; ++k)
@@ -438,10 +431,6 @@ static bool lut2_ok(const LutParams& p) {
 }
 
 void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream) {
-    if (b1_supported(p)) {
-        b1_launch(p, X, out, stream);
-        return;
-    }
     if (lut2_ok(p)) {
         switch (p.cols) {
             case 4096: lut2_launch_t<128>(p, X, out, stream); break;
@@ -455,15 +444,8 @@ void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stre
         BD_CUDA(cudaGetLastError());
         return;
     }
-    // compile-time row strides for the published shapes (immediate load offsets)
-    switch (p.cols) {
-        case 4096: lut_launch_t<128>(p, X, out, stream); break;
-        case 8192: lut_launch_t<256>(p, X, out, stream); break;
-        case 11008: lut_launch_t<344>(p, X, out, stream); break;
-        case 14336: lut_launch_t<448>(p, X, out, stream); break;
-        case 28672: lut_launch_t<896>(p, X, out, stream); break;
-        default: lut_launch_t<0>(p, X, out, stream); break;
-    }
+    // v1 (cols % 32 == 0 but not % 128: no published shape) with a runtime row stride
+    lut_launch_t<0>(p, X, out, stream);
     note_launch();
     BD_CUDA(cudaGetLastError());
 }

@@ -130,13 +130,6 @@ __device__ __forceinline__ uint32_t expand4(uint32_t w, int c) {
     return ((w << (3 - c)) & 0x88888888u) ^ 0xAAAAAAAAu;
 }
 
-__device__ __forceinline__ void trace(const Mt4Params& p, int role, int i) {
-    if (p.trace && blockIdx.x == 0 && i < 512 && role < 8) {
-        long long t;
-        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
-        p.trace[role * 512 + i] = t;
-    }
-}
 
 // Stage cursor over a per-tile schedule table (built on the host, kept in smem).
 // Inside a tile the backbone stages are spread evenly among the plane stages
@@ -274,14 +267,16 @@ __global__ void __launch_bounds__(kThreads, 1) mt4_kernel(const __grid_constant_
             const uint32_t lap = nfill[ri]++ / uint32_t(c.base ? p.ring_b : p.ring_p);
             const int si = (c.base ? 0 : kMaxRingB) + s;
             if (k != prod) continue;
-            if (lane == 0)
-                while (slot_fills[si] != lap) {
-                }
+            if (lane == 0) {
+                // acquire: the previous fill of this slot (another producer warp) was issued
+                uint32_t spins = 0;
+                while (ld_acquire_cta(&slot_fills[si]) != lap)
+                    if (++spins == (1u << 30)) __trap();  // schedule bug: fault instead of hanging
+            }
             __syncwarp();
             const int m0 = c.tile * 128;
             if (c.base) {
                 mbar_wait_w(&empty_b[s], ph ^ 1);
-                if (prod == 0) trace(p, 0, int(c.g - g0));
                 uint8_t* sp = smem + s * L.bstage;
                 mbar_arrive_expect_tx_w(&full_b[s], kStageMain + p.bn * 128);
                 const int kc = c.chunk * kBaseCols;
@@ -289,14 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1) mt4_kernel(const __grid_constant_
                 tma_load_2d_w(sp + L.aux_off, &p.map_x, &full_b[s], kc, 0, pol_keep);
             } else {
                 mbar_wait_w(&empty_p[s], ph ^ 1);
-                if (prod == 0) trace(p, 0, int(c.g - g0));
                 uint8_t* sp = smem + L.pring_off + s * L.pstage;
-                if (p.debug & 8) {
-                    mbar_arrive_w(&full_p[s]);
-                    __syncwarp();
-                    if (lane == 0) slot_fills[si] = lap + 1;
-                    continue;
-                }
                 const Mt4Slot& sl = p.slots[c.slot];
                 int sub = 0;
                 while (sub + 1 < p.n_subs && m0 >= p.sub_row0[sub + 1]) ++sub;
@@ -309,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1) mt4_kernel(const __grid_constant_
                                 &full_p[s], pol_keep);
             }
             __syncwarp();
-            if (lane == 0) slot_fills[si] = lap + 1;  // the slot's next fill may now be armed
+            if (lane == 0) st_release_cta(&slot_fills[si], lap + 1);  // the slot's next fill may now be armed
         }
     } else if (warp == 16) {
         // ---- backbone MMA issuer (whole warp, one elected lane issues) ----
@@ -329,11 +317,10 @@ __global__ void __launch_bounds__(kThreads, 1) mt4_kernel(const __grid_constant_
                 tc_fence_after();
             }
             const uint64_t da = sdesc_k128(sp), db = sdesc_k128(sp + L.aux_off);
-            if (!(p.debug & 4))
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                    mma_bf16_ss_w(tbase + p.col_base, da + 2 * kk, db + 2 * kk, id_base,
-                                  (c.first && kk == 0) ? 0u : 1u);
+            for (int kk = 0; kk < 4; ++kk)
+                mma_bf16_ss_w(tbase + p.col_base, da + 2 * kk, db + 2 * kk, id_base,
+                              (c.first && kk == 0) ? 0u : 1u);
             tc_commit_w(&empty_b[s]);
             if (c.last) {
                 tc_commit_w(base_full);
@@ -350,7 +337,6 @@ __global__ void __launch_bounds__(kThreads, 1) mt4_kernel(const __grid_constant_
             if (c.base) continue;
             const int s = rp.i;
             mbar_wait_w(&full_p[s], rp.ph);
-            trace(p, 1, int(c.g - g0));
             uint8_t* sp = smem + L.pring_off + s * L.pstage;
             const Mt4Slot& sl = p.slots[c.slot];
             if (c.first) mbar_wait_w(&acc_empty[acc.i], acc.ph ^ 1);
@@ -360,22 +346,19 @@ __global__ void __launch_bounds__(kThreads, 1) mt4_kernel(const __grid_constant_
             const uint64_t db = sdesc_sw128(sp + L.aux_off, kAuxReq);
             const uint32_t xstep = 1024u >> 4;  // descriptor units (16 B)
             mbar_wait_w(&a_full[ring.i], ring.ph);
-            trace(p, 5, int(c.g - g0));
             tc_fence_after();
             const uint32_t ent0 = tbase + p.col_ring + ring.i * kStageCols;
-            if (!(p.debug & 2))
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const uint32_t ent = ent0 + j * kEntryCols;
-                    const uint64_t db0 = db + j * xstep;
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t ent = ent0 + j * kEntryCols;
+                const uint64_t db0 = db + j * xstep;
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)
-                        mma_mxf4_ts_w(d, ent + 8 + 8 * kk, db0 + 2 * kk, idesc | (uint32_t(2 * (kk & 1)) << 4),
-                                      tbase + p.col_sfa, ent + 2 * (kk >> 1), (c.first && j == 0 && kk == 0) ? 0u : 1u);
-                }
+                for (int kk = 0; kk < 4; ++kk)
+                    mma_mxf4_ts_w(d, ent + 8 + 8 * kk, db0 + 2 * kk, idesc | (uint32_t(2 * (kk & 1)) << 4),
+                                  tbase + p.col_sfa, ent + 2 * (kk >> 1), (c.first && j == 0 && kk == 0) ? 0u : 1u);
+            }
             tc_commit_w(&a_empty[ring.i]);
             ring.next(p.n_ring);
-            trace(p, 2, int(c.g - g0));
             tc_commit_w(&empty_p[s]);
             if (c.last) {
                 tc_commit_w(&acc_full[acc.i]);
@@ -415,7 +398,6 @@ __global__ void __launch_bounds__(kThreads, 1) mt4_kernel(const __grid_constant_
                 ring.next(p.n_ring);
                 continue;
             }
-            if (trow == 0) trace(p, 3, int(c.g - g0));
             const Mt4Slot& sl = p.slots[c.slot];
             const uint8_t* sp = smem + L.pring_off + s * L.pstage;
             const uint8_t* rowp = sp + trow * 128;
@@ -433,19 +415,16 @@ __global__ void __launch_bounds__(kThreads, 1) mt4_kernel(const __grid_constant_
                     sc[2] = v.y;
                 }
                 tmem_st4(ent, sc);
-                if (!(p.debug & 1)) {
-                    const uint4 v0 = *reinterpret_cast<const uint4*>(rowp + (((2 * j) ^ sw) << 4));
-                    const uint4 v1 = *reinterpret_cast<const uint4*>(rowp + (((2 * j + 1) ^ sw) << 4));
-                    const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-                    uint32_t a[32];
+                const uint4 v0 = *reinterpret_cast<const uint4*>(rowp + (((2 * j) ^ sw) << 4));
+                const uint4 v1 = *reinterpret_cast<const uint4*>(rowp + (((2 * j + 1) ^ sw) << 4));
+                const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+                uint32_t a[32];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u)
+                for (int u = 0; u < 8; ++u)
 #pragma unroll
-                        for (int cc = 0; cc < 4; ++cc) a[4 * u + cc] = expand4(w[u], cc);
-                    tmem_st32(ent + 8, a);
-                }
+                    for (int cc = 0; cc < 4; ++cc) a[4 * u + cc] = expand4(w[u], cc);
+                tmem_st32(ent + 8, a);
             }
-            if (trow == 0) trace(p, 7, int(c.g - g0));
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
@@ -454,7 +433,6 @@ __global__ void __launch_bounds__(kThreads, 1) mt4_kernel(const __grid_constant_
                 mbar_arrive(&empty_p[s]);
             }
             ring.next(p.n_ring);
-            if (trow == 0) trace(p, 4, int(c.g - g0));
         }
     } else if (warp >= 12 && warp < 16) {
         // ---- epilogue: thread = tile row ----
@@ -672,8 +650,6 @@ bool plan_mt4(Mt4Params& p, uint64_t M, uint64_t K, int batch) {
     if (p.n_ring < 2) return false;
     p.ring_b = rb;
     p.ring_p = rp;
-    p.debug = std::getenv("BD_MT4_DEBUG") ? std::atoi(std::getenv("BD_MT4_DEBUG")) : 0;
-    p.trace = nullptr;
     p.smem = int(mt4_layout(p.bn, p.nr_max, rb, rp).total);
     // splits = most CTAs covering one tile
     auto cta_of_h = [&](long long s) {

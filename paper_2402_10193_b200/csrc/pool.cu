@@ -150,18 +150,11 @@ struct Plan {
     std::vector<DeltaUnit> lm_units;
     GemmPlan g_qkv, g_o, g_gu, g_down, g_lm;
     CUtensorMap x_xn, x_ctx, x_act;  // B-operand maps for this batch size
-    // fused K2+K3 (tensor-core deltas) per layer & group, when eligible
-    struct Fused {
-        bool ok = false;
-        FusedParams prm;
-    };
-    std::vector<std::array<Fused, 4>> fused;
-    // byte-LUT deltas (few requests per tenant) per layer & group
+    // byte-LUT deltas (few requests per tenant) per layer & group; one launch per
+    // kLutMaxJobs requests (each launch writes its own requests' rows of D)
     struct Lut {
         bool ok = false;
-        LutParams prm;
-        bool mxd = false;  // K3t (FP4 tensor cores) instead of the byte LUT for this group
-        MxdParams mx;
+        std::vector<LutParams> prm;
     };
     std::vector<std::array<Lut, 4>> lut;
     // K23 (base + FP4 tensor-core deltas in one kernel) per layer & group
@@ -171,12 +164,6 @@ struct Plan {
     };
     std::vector<std::array<M4, 4>> mt4;
     uint8_t* xpk = nullptr;  // FP4 activation pieces + scales [B][chunks][kXpBlock]
-    int8_t* Xq = nullptr;  // [256 x ldq] int8 pieces (zero padded)
-    int ldq = 0;
-    float* xscale = nullptr;
-    int* qsum = nullptr;
-    int* d_xq_row = nullptr;
-    CUtensorMap m_xq_dim, m_xq_inter;
     cudaGraphExec_t graph_layers = nullptr, graph_full = nullptr;
     uint64_t kernels_layers = 0, kernels_full = 0;
 };
@@ -225,14 +212,11 @@ struct PoolImpl {
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     cudaStream_t stream2 = nullptr;  // side stream: K2 beside K3
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    bool concurrent_k23 = true;      // BD_SERIAL=1 disables
-    bool pdl_edges = true;           // BD_PDL_EDGES=0 keeps captured cross-stream edges full
+    bool concurrent_k23 = true;      // K2 beside the LUT (false only inside a serial profile)
     bool use_graphs = true;
-    // timing experiments only (results are wrong): BD_SKIP bitmask drops launches of
-    // 1 norm, 2 attention, 4 silu, 8 K3 delta, 16 K2 gemm
-    int skip = 0;
-    bool use_fused = true;
-    std::string delta_mode = "auto";  // auto | lut | fused | units (BD_DELTA)
+    // auto | lut | mt4 | units; BD_DELTA forces one K3 variant (test hook: every variant is
+    // checked against the oracle on the same inputs)
+    std::string delta_mode = "auto";
 
     ~PoolImpl() {
         cudaSetDevice(device);
@@ -300,14 +284,8 @@ struct PoolImpl {
         BD_CUDA(cudaStreamCreateWithFlags(&stream2, cudaStreamNonBlocking));
         BD_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
         BD_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-        if (const char* e = std::getenv("BD_SERIAL")) concurrent_k23 = (e[0] == '0');
-        if (const char* e = std::getenv("BD_PDL_EDGES")) pdl_edges = (e[0] != '0');
         BD_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         BD_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
-        if (const char* e = std::getenv("BD_NO_GRAPH")) use_graphs = (e[0] == '0');
-        if (const char* e = std::getenv("BD_SKIP")) skip = std::atoi(e);
-        if (const char* e = std::getenv("BD_NO_FUSED")) use_fused = (e[0] == '0');
-        if (!use_fused) delta_mode = "units";
         if (const char* e = std::getenv("BD_DELTA")) delta_mode = e;
 
         L.resize(a.n_layers);
@@ -744,7 +722,6 @@ struct PoolImpl {
     void plan_lut_groups(Plan& p) {
         const int B = p.B;
         const uint64_t nL = a.n_layers;
-        if (B > kLutMaxJobs) return;
         p.lut.assign(nL, {});
         struct GroupDef {
             std::vector<int> projs;
@@ -764,100 +741,30 @@ struct PoolImpl {
             }
             bool ok = true;
             for (uint64_t l = 0; l < nL && ok; ++l) {
-                LutParams prm{};
-                prm.n_jobs = B;
-                for (int b = 0; b < B; ++b) {
-                    LutJob& j = prm.jobs[b];
-                    j.req = b;
-                    const Tenant& t = tenants[requests[p.reqs[b]].tenant];
-                    for (size_t s = 0; s < gd.projs.size(); ++s) {
-                        const auto& planes = t.proj[l][gd.projs[s]];
-                        j.n_planes[s] = int(planes.size());
-                        for (size_t k = 0; k < planes.size(); ++k) {
-                            j.bits[s][k] = planes[k].bits;
-                            j.alpha[s][k] = planes[k].alpha;
+                for (int b0 = 0; b0 < B && ok; b0 += kLutMaxJobs) {
+                    LutParams prm{};
+                    prm.n_jobs = std::min(kLutMaxJobs, B - b0);
+                    for (int q = 0; q < prm.n_jobs; ++q) {
+                        LutJob& j = prm.jobs[q];
+                        j.req = b0 + q;
+                        const Tenant& t = tenants[requests[p.reqs[b0 + q]].tenant];
+                        for (size_t s = 0; s < gd.projs.size(); ++s) {
+                            const auto& planes = t.proj[l][gd.projs[s]];
+                            j.n_planes[s] = int(planes.size());
+                            for (size_t k = 0; k < planes.size(); ++k) {
+                                j.bits[s][k] = planes[k].bits;
+                                j.alpha[s][k] = planes[k].alpha;
+                            }
                         }
                     }
+                    ok = plan_lut(prm, seg_rows, int(gd.projs.size()), int(gd.cols), int(gd.ldx), B);
+                    if (ok && size_t(prm.slices) * B * prm.M > D_elems) ok = false;
+                    if (ok) p.lut[l][gi].prm.push_back(prm);
                 }
-                ok = plan_lut(prm, seg_rows, int(gd.projs.size()), int(gd.cols), int(gd.ldx), B);
-                if (ok && size_t(prm.slices) * B * prm.M > D_elems) ok = false;
-                if (ok) {
-                    p.lut[l][gi].prm = prm;
-                    p.lut[l][gi].ok = true;
-                }
+                p.lut[l][gi].ok = ok;
             }
             if (!ok)
-                for (uint64_t l = 0; l < nL; ++l) p.lut[l][gi].ok = false;
-        }
-        plan_mxd_groups(p);
-    }
-
-    // K3t (mxd.cu) for the LUT-planned groups: one plane per (request, segment), 128-row
-    // aligned segments; the plane tensor maps live in one device table per plan
-    void plan_mxd_groups(Plan& p) {
-        const int B = p.B;
-        const uint64_t nL = a.n_layers;
-        std::vector<CUtensorMap> maps;
-        std::vector<std::pair<uint64_t, int>> users;  // (layer, group) -> first map index
-        std::vector<size_t> first;
-        for (int gi = 0; gi < 4; ++gi) {
-            if (nL == 0 || !p.lut[0][gi].ok) continue;
-            {   // shape checks before any tensor map is encoded (TMA needs 16-byte row strides)
-                MxdParams probe{};
-                probe.n_jobs = 1;
-                const LutParams& lp = p.lut[0][gi].prm;
-                int seg_rows[kLutMaxSegs];
-                for (int sg = 0; sg < lp.n_segs; ++sg) seg_rows[sg] = lp.seg_row0[sg + 1] - lp.seg_row0[sg];
-                if (!plan_mxd(probe, seg_rows, lp.n_segs, lp.cols, B)) continue;
-            }
-            bool ok = true;
-            std::vector<size_t> idx(nL);
-            std::vector<MxdParams> prms(nL);
-            for (uint64_t l = 0; l < nL && ok; ++l) {
-                const LutParams& lp = p.lut[l][gi].prm;
-                MxdParams& m = prms[l];
-                m = MxdParams{};
-                m.n_jobs = lp.n_jobs;
-                int seg_rows[kLutMaxSegs];
-                for (int sg = 0; sg < lp.n_segs; ++sg) seg_rows[sg] = lp.seg_row0[sg + 1] - lp.seg_row0[sg];
-                idx[l] = maps.size();
-                for (int j = 0; j < lp.n_jobs && ok; ++j) {
-                    m.jobs[j].req = lp.jobs[j].req;
-                    for (int sg = 0; sg < lp.n_segs; ++sg) {
-                        if (lp.jobs[j].n_planes[sg] != 1 ||
-                            reinterpret_cast<uintptr_t>(lp.jobs[j].bits[sg][0]) % 16) {
-                            ok = false;
-                            break;
-                        }
-                        m.jobs[j].alpha[sg] = lp.jobs[j].alpha[sg][0];
-                        maps.push_back(tmap_bits4(lp.jobs[j].bits[sg][0], uint64_t(seg_rows[sg]), uint64_t(lp.cols)));
-                    }
-                }
-                ok = ok && plan_mxd(m, seg_rows, lp.n_segs, lp.cols, B);
-            }
-            if (!ok) {
-                maps.resize(idx.empty() ? maps.size() : idx[0]);
-                continue;
-            }
-            for (uint64_t l = 0; l < nL; ++l) {
-                p.lut[l][gi].mx = prms[l];
-                p.lut[l][gi].mxd = true;
-                first.push_back(idx[l]);
-                users.push_back({l, gi});
-            }
-        }
-        if (users.empty()) return;
-        CUtensorMap* d = dmalloc<CUtensorMap>(maps.size(), &p.allocs);
-        BD_CUDA(cudaMemcpy(d, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
-        const int max_chunks = xp_chunks(int(std::max(a.dim, a.intermediate)));
-        if (!p.xpk) {
-            p.xpk = dmalloc<uint8_t>(size_t(B) * max_chunks * kXpBlock, &p.allocs);
-            BD_CUDA(cudaMemset(p.xpk, 0, size_t(B) * max_chunks * kXpBlock));
-        }
-        for (size_t u = 0; u < users.size(); ++u) {
-            MxdParams& m = p.lut[users[u].first][users[u].second].mx;
-            m.maps = d + first[u];
-            m.xpk = p.xpk;
+                for (uint64_t l = 0; l < nL; ++l) p.lut[l][gi] = Plan::Lut{};
         }
     }
 
@@ -964,113 +871,6 @@ struct PoolImpl {
                 for (uint64_t l = 0; l < nL; ++l) p.mt4[l][gi].ok = false;
         }
         (void)any;
-    }
-
-    // Tensor-core delta path (mtfused.cu) for every projection group whose
-    // shapes allow it (plane rows start on 16-byte TMA boundaries: cols % 128,
-    // stacked sub-matrix boundaries % 128) and whose slots fit TMEM.
-    void plan_fused_groups(Plan& p, const std::vector<int>& order,
-                           std::map<int, std::vector<int>>& by_t) {
-        const int B = p.B;
-        const uint64_t nL = a.n_layers;
-        // Xq rows: each tenant's requests get consecutive rows, 8-row aligned
-        std::vector<int> xq_row(B, 0), t_xrow;
-        int rows = 0;
-        for (int t : order) {
-            const auto& rq = by_t[t];
-            for (size_t c = 0; c < rq.size(); c += kFusedMaxReq) {
-                const int n = int(std::min<size_t>(kFusedMaxReq, rq.size() - c));
-                t_xrow.push_back(rows);
-                for (int q = 0; q < n; ++q) xq_row[rq[c + q]] = rows + 2 * q;
-                const int mma_n = 2 * n <= 8 ? 8 : ((2 * n + 15) / 16) * 16;
-                rows += ((std::max(2 * n, 8) + 7) / 8) * 8;
-                (void)mma_n;
-            }
-        }
-        const uint64_t kpad = round_up(std::max(a.dim, a.intermediate), kFusedBK);
-        p.ldq = int(kpad);
-        const int xq_alloc_rows = 256 + 16;
-        p.Xq = dmalloc<int8_t>(size_t(xq_alloc_rows) * kpad, &p.allocs);
-        BD_CUDA(cudaMemset(p.Xq, 0, size_t(xq_alloc_rows) * kpad));
-        p.xscale = dmalloc<float>(B, &p.allocs);
-        p.qsum = dmalloc<int>(size_t(B) * 2 * (kpad / kFusedBK + 1), &p.allocs);
-        p.d_xq_row = dmalloc<int>(B, &p.allocs);
-        BD_CUDA(cudaMemcpy(p.d_xq_row, xq_row.data(), B * sizeof(int), cudaMemcpyHostToDevice));
-        p.fused.assign(nL, {});
-        struct GroupDef {
-            std::vector<int> projs;
-            uint64_t cols;
-            const CUtensorMap* mx;
-        };
-        const GroupDef defs[4] = {{{P_Q, P_K, P_V}, a.dim, &p.x_xn},
-                                  {{P_O}, a.dim, &p.x_ctx},
-                                  {{P_GATE, P_UP}, a.dim, &p.x_xn},
-                                  {{P_DOWN}, a.intermediate, &p.x_act}};
-        for (int gi = 0; gi < 4; ++gi) {
-            const GroupDef& gd = defs[gi];
-            if (gd.cols % 128) continue;
-            if (!p.lut.empty() && p.lut[0][gi].ok) continue;  // LUT path already chosen
-            if (!p.mt4.empty() && p.mt4[0][gi].ok) continue;  // K23 already chosen
-            bool ok = true;
-            uint64_t M = 0;
-            std::vector<int> sub_row0;
-            for (int pj : gd.projs) {
-                uint64_t r0, nr;
-                local_rows(pj, r0, nr);
-                if (nr % 128) ok = false;
-                sub_row0.push_back(int(M));
-                M += nr;
-            }
-            sub_row0.push_back(int(M));
-            if (!ok) continue;
-            for (uint64_t l = 0; l < nL && ok; ++l) {
-                FusedParams prm{};
-                prm.n_subs = int(gd.projs.size());
-                for (size_t s = 0; s < sub_row0.size(); ++s) prm.sub_row0[s] = sub_row0[s];
-                std::vector<CUtensorMap> maps;
-                int slot = 0, ti = 0;
-                for (int t : order) {
-                    const auto& rq = by_t[t];
-                    const size_t n_planes = tenants[t].proj[l][gd.projs[0]].size();
-                    for (size_t c = 0; c < rq.size() && ok; c += kFusedMaxReq, ++ti) {
-                        for (size_t k = 0; k < n_planes; ++k) {
-                            if (slot >= kFusedMaxSlots) { ok = false; break; }
-                            FusedSlot& fs = prm.slots[slot++];
-                            fs.n_req = int(std::min<size_t>(kFusedMaxReq, rq.size() - c));
-                            for (int q = 0; q < fs.n_req; ++q) fs.req[q] = rq[c + q];
-                            fs.xrow = t_xrow[ti];
-                            for (size_t s = 0; s < gd.projs.size(); ++s) {
-                                const int pj = gd.projs[s];
-                                const auto& planes = tenants[t].proj[l][pj];
-                                if (planes.size() != n_planes) { ok = false; break; }
-                                uint64_t r0, nr;
-                                local_rows(pj, r0, nr);
-                                fs.alpha[s] = planes[k].alpha;
-                                fs.map_idx[s] = int(maps.size());
-                                maps.push_back(tmap_bits(planes[k].bits, nr, gd.cols));
-                            }
-                        }
-                    }
-                }
-                prm.n_slots = slot;
-                if (!ok || !plan_fused(prm, M, gd.cols, B)) { ok = false; break; }
-                CUtensorMap* dm = dmalloc<CUtensorMap>(maps.size(), &p.allocs);
-                BD_CUDA(cudaMemcpy(dm, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
-                prm.bits_maps = dm;
-                prm.map_x = *gd.mx;
-                const LayerW& W = L[l];
-                prm.map_w = gi == 0 ? W.m_qkv : gi == 1 ? W.m_o : gi == 2 ? W.m_gu : W.m_down;
-                prm.map_xq = tmap_xq(p.Xq, prm.xq_rows, round_up(gd.cols, kFusedBK), kpad);
-                prm.xscale = p.xscale;
-                prm.qsum = p.qsum;
-                prm.partial = P;
-                require(uint64_t(prm.splits) * B * M <= P_elems, BD_ERR_CUDA, "split-K workspace too small");
-                p.fused[l][gi].prm = prm;
-                p.fused[l][gi].ok = true;
-            }
-            if (!ok)
-                for (uint64_t l = 0; l < nL; ++l) p.fused[l][gi].ok = false;
-        }
     }
 
     Plan& plan_for(const std::vector<int>& reqs) {
@@ -1187,36 +987,30 @@ struct PoolImpl {
         p->x_xn = tmap_acts(xn, B, a.dim, ld_dim, bn);
         p->x_ctx = tmap_acts(ctx, B, a.dim, ld_dim, bn);
         p->x_act = tmap_acts(act, B, a.intermediate, ld_inter, bn);
-        size_t max_per_tenant = 0;
-        for (int t : order) max_per_tenant = std::max(max_per_tenant, by_t[t].size());
-        // K23 (mt4) when forced, or by default for tenants with many requests each
-        // (the byte-LUT beside K2 is measured faster at one request per tenant)
-        // K23 from 4 requests per tenant (plane read once per slot of 4 requests; Mistral-7B
-        // sweep at batch 64: +30 % at 4 requests/tenant); the byte LUT otherwise
-        if (delta_mode == "mt4" || (delta_mode == "auto" && int(max_per_tenant) >= k23_min_requests(B)))
+        // K3 variant for the whole batch (one backend, chosen by requests per tenant): K23
+        // when tenants average k23_min_requests(B) requests or more (each plane is then read
+        // once per slot of up to 4 requests), the byte LUT beside K2 otherwise (one job per
+        // request); the mean, not the maximum, so one busy tenant does not move a batch of
+        // single-request tenants onto K23 (measured slower there)
+        const double mean_per_tenant = order.empty() ? 0.0 : double(B) / double(order.size());
+        if (delta_mode == "mt4" || (delta_mode == "auto" && mean_per_tenant >= k23_min_requests(B)))
             plan_mt4_groups(*p, by_t);
         if (delta_mode == "lut" || delta_mode == "auto") plan_lut_groups(*p);
-        // groups already served by K23 keep neither LUT nor fused plans
+        // groups already served by K23 keep no LUT plan
         for (uint64_t l = 0; l < p->mt4.size(); ++l)
             for (int gi = 0; gi < 4; ++gi)
-                if (p->mt4[l][gi].ok && !p->lut.empty()) p->lut[l][gi].ok = false;
-        if (concurrent_k23 && !p->lut.empty()) {
+                if (p->mt4[l][gi].ok && !p->lut.empty()) p->lut[l][gi] = Plan::Lut{};
+        if (!p->lut.empty()) {
             // K2 runs beside the K3 LUT on every SM: one GEMM CTA per SM within the
             // shared memory the LUT leaves (LUT: 132 KB + 512 threads x 96 regs)
             GemmPlan* gs[4] = {&p->g_qkv, &p->g_o, &p->g_gu, &p->g_down};
-            // (the opt-in binary tensor-core K3b needs only 3.3 KB of shared memory: K2 takes the rest)
-            static const int b1_cap = 190;
             for (int gi = 0; gi < 4; ++gi)
                 if (p->lut[0][gi].ok) {
-                    int cap = b1_supported(p->lut[0][gi].prm) ? b1_cap * 1024 : 88 * 1024;
-                    static const char* cap3 = std::getenv("BD_K2_CAP_DOWN");
-                    if (gi == 3 && cap3) cap = std::atoi(cap3) * 1024;
-                    *gs[gi] = plan_base_gemm(gs[gi]->M, gs[gi]->K, B, cap);
+                    *gs[gi] = plan_base_gemm(gs[gi]->M, gs[gi]->K, B, 88 * 1024);
                     require(uint64_t(gs[gi]->splits) * B * gs[gi]->M <= P_elems, BD_ERR_CUDA,
                             "split-K workspace too small");
                 }
         }
-        if (delta_mode == "fused" || delta_mode == "auto") plan_fused_groups(*p, order, by_t);
         auto& slot = plans[key];
         slot = std::move(p);
         return *slot;
@@ -1253,9 +1047,6 @@ struct PoolImpl {
         prof_events.push_back({kind, {e0, e1}});
     }
 
-    bool fused_ok(const Plan& p, uint64_t l, int gi) const {
-        return p.fused.size() > l && p.fused[l][gi].ok;
-    }
     bool lut_ok(const Plan& p, uint64_t l, int gi) const { return p.lut.size() > l && p.lut[l][gi].ok; }
     bool mt4_ok(const Plan& p, uint64_t l, int gi) const { return p.mt4.size() > l && p.mt4[l][gi].ok; }
     ProjOut group_out(const Plan& p, uint64_t l, int gi, const GemmPlan& g) const {
@@ -1271,17 +1062,7 @@ struct PoolImpl {
         }
         if (lut_ok(p, l, gi)) {
             ProjOut o = proj_out(g, true);
-            o.dsplits = p.lut[l][gi].prm.slices;
-            return o;
-        }
-        if (fused_ok(p, l, gi)) {
-            const FusedParams& f = p.fused[l][gi].prm;
-            ProjOut o;
-            o.P = P;
-            o.splits = f.splits;
-            o.pstride = size_t(p.B) * f.M;
-            o.D = nullptr;
-            o.M = f.M;
+            o.dsplits = p.lut[l][gi].prm[0].slices;
             return o;
         }
         return proj_out(g, true);
@@ -1296,37 +1077,26 @@ struct PoolImpl {
             return;
         }
         if (lut_ok(p, l, group)) {
+            const auto& luts = p.lut[l][group].prm;
             if (concurrent_k23) {
                 // K3 (CUDA cores / LSU) and K2 (TMA + tensor pipe) share every SM:
                 // fork the GEMM onto the side stream, join before the consumer.
                 // Profiled as one unit (kind FUSED_*: all of K2+K3 for the group).
                 prof(BD_PROF_FUSED_QKV + group, s, [&] {
-                    // K3t: the FP4 pieces first, so the delta kernel (PDL) claims its SM
-                    // slots before K2 (side stream) could take two CTAs per SM
-                    const bool mxd = p.lut[l][group].mxd && !(skip & 8);
-                    if (mxd) xp_prep_launch(X, ldx, cols, B, p.xpk, s);
                     BD_CUDA(cudaEventRecord(ev_fork, s));
                     BD_CUDA(cudaStreamWaitEvent(stream2, ev_fork, 0));
-                    if (mxd)
-                        mxd_launch(p.lut[l][group].mx, D, s);
-                    else if (!(skip & 8))
-                        lut_launch(p.lut[l][group].prm, X, D, s);
-                    if (!(skip & 16)) base_gemm_launch(g, mw, mx, P, stream2);
+                    for (const LutParams& lp : luts) lut_launch(lp, X, D, s);
+                    base_gemm_launch(g, mw, mx, P, stream2);
                     BD_CUDA(cudaEventRecord(ev_join, stream2));
                     BD_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
                 });
                 return;
             }
+            // serial (profile_layers_serial): K2 and K3 timed on their own
             prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm_launch(g, mw, mx, P, s); });
-            prof(BD_PROF_DELTA_QKV + group, s, [&] { lut_launch(p.lut[l][group].prm, X, D, s); });
-            return;
-        }
-        if (fused_ok(p, l, group)) {
-            const FusedParams& f = p.fused[l][group].prm;
-            prof(BD_PROF_XQ_PREP, s, [&] {
-                xq_prep_launch(X, ldx, cols, B, p.d_xq_row, p.Xq, p.ldq, p.xscale, p.qsum, f.kb_total, s);
+            prof(BD_PROF_DELTA_QKV + group, s, [&] {
+                for (const LutParams& lp : luts) lut_launch(lp, X, D, s);
             });
-            prof(BD_PROF_FUSED_QKV + group, s, [&] { fused_launch(f, s); });
             return;
         }
         prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm_launch(g, mw, mx, P, s); });
@@ -1388,13 +1158,13 @@ struct PoolImpl {
         for (uint64_t l = 0; l < nL; ++l) {
             const LayerW& W = L[l];
             // x += down(prev); xn = norm1(x)   (x and xn replicated on every rank)
-            if (!(skip & 1)) prof(BD_PROF_NORM, s, [&] {
+            prof(BD_PROF_NORM, s, [&] {
                 resid_norm_launch(x, B, int(a.dim), prev, p.d_norm + (2 * l) * B, xn, int(ld_dim),
                                   nullptr, msq, s);
             });
             linear(p, l, 0, p.g_qkv, W.m_qkv, p.x_xn, p.units[l][0], xn, int(ld_dim), int(a.dim), B, s);
             aa.layer = int(l);
-            if (!(skip & 2)) prof(BD_PROF_ATTN, s, [&] {
+            prof(BD_PROF_ATTN, s, [&] {
                 attn_launch(group_out(p, l, 0, p.g_qkv), aa, p.d_pos, B, tp ? ctx_loc : ctx,
                             tp ? int(q_l) : int(ld_dim), s);
             });
@@ -1402,12 +1172,12 @@ struct PoolImpl {
             linear(p, l, 1, p.g_o, W.m_o, p.x_ctx, p.units[l][1], ctx, int(ld_dim), int(a.dim), B, s);
             const ProjOut o_out = tp ? exchange_f32(group_out(p, l, 1, p.g_o), B, int(dim_l), s)
                                      : group_out(p, l, 1, p.g_o);
-            if (!(skip & 1)) prof(BD_PROF_NORM, s, [&] {
+            prof(BD_PROF_NORM, s, [&] {
                 resid_norm_launch(x, B, int(a.dim), o_out, p.d_norm + (2 * l + 1) * B, xn, int(ld_dim),
                                   nullptr, msq, s);
             });
             linear(p, l, 2, p.g_gu, W.m_gu, p.x_xn, p.units[l][2], xn, int(ld_dim), int(a.dim), B, s);
-            if (!(skip & 4)) prof(BD_PROF_SILU, s, [&] {
+            prof(BD_PROF_SILU, s, [&] {
                 silu_launch(group_out(p, l, 2, p.g_gu), B, int(inter_l), tp ? act_loc : act,
                             tp ? int(inter_l) : int(ld_inter), s);
             });
@@ -1436,15 +1206,13 @@ struct PoolImpl {
     }
 
     // K3 variant per projection group (q/k/v, o, gate/up, down) of layer 0 of plan p:
-    // T = K23 (FP4 tensor cores, fused with K2), L = byte LUT beside K2, X = K3t beside K2,
-    // F = i8 tensor-core fused kernel, U = SIMT units
+    // T = K23 (FP4 tensor cores, fused with K2), L = byte LUT beside K2, U = SIMT units
     void record_paths(const Plan& p) {
         for (int gi = 0; gi < 4; ++gi) {
             char c = 'U';
             if (a.n_layers == 0) c = '-';
             else if (mt4_ok(p, 0, gi)) c = 'T';
-            else if (lut_ok(p, 0, gi)) c = p.lut[0][gi].mxd ? 'X' : 'L';
-            else if (fused_ok(p, 0, gi)) c = 'F';
+            else if (lut_ok(p, 0, gi)) c = 'L';
             stats.delta_paths[gi] = c;
         }
         stats.delta_paths[4] = 0;
@@ -1492,7 +1260,7 @@ struct PoolImpl {
             }
             BD_CUDA(cudaStreamEndCapture(stream, &graph));
             kcount = launch_count() - c0;
-            if (pdl_edges) promote_programmatic_edges(graph);
+            promote_programmatic_edges(graph);
             BD_CUDA(cudaGraphInstantiate(&g, graph, 0));
             BD_CUDA(cudaGraphDestroy(graph));
         }
@@ -1662,21 +1430,24 @@ void pool_decode_layers(bd_pool* p, const bd_request* r, uint64_t n, const float
     p->impl.step(r, n, false, xin, xout, nullptr, static_cast<cudaStream_t>(s));
 }
 void pool_profile_layers(bd_pool* p, const bd_request* r, uint64_t n, const float* xin,
-                         float* xout, double* ms, uint64_t* cnt, void* s) {
+                         float* xout, double* ms, uint64_t* cnt, void* s, bool serial) {
     require((r && xin && xout && ms && cnt) || n == 0, BD_ERR_BAD_ARGUMENT,
             "profile_layers: null argument");
     PoolImpl& P = p->impl;
     P.validate(r, n);
     P.profiling = true;
+    P.concurrent_k23 = !serial;
     P.prof_events.clear();
     try {
         P.stats.backbone_passes += 1;
         P.step(r, n, false, xin, xout, nullptr, static_cast<cudaStream_t>(s));
     } catch (...) {
         P.profiling = false;
+        P.concurrent_k23 = true;
         throw;
     }
     P.profiling = false;
+    P.concurrent_k23 = true;
     BD_CUDA(cudaStreamSynchronize(P.stream));
     for (int k = 0; k < BD_PROF_KINDS; ++k) {
         ms[k] = 0.0;

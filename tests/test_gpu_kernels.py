@@ -211,10 +211,10 @@ def test_multitenant_linear_delta_only(cuda, rows, cols, B, T):
     assert _delta_only_case(rows, cols, B, T, cuda) <= 1e-5
 
 
-@pytest.mark.parametrize("mode", ["mt4", "lut", "lut-b1"])
+@pytest.mark.parametrize("mode", ["mt4", "lut", "units"])
 def test_multitenant_linear_delta_only_each_path(cuda, mode):
     """Delta term alone through K23 (FP4 pieces, ~1e-7 measured), the byte LUT and the
-    opt-in binary tensor-core variant of the LUT plan (K3b, exact integer reconstruction)."""
+    SIMT units."""
     import subprocess
     import sys
 
@@ -229,7 +229,7 @@ for case in [(4096, 4096, 16, 16), (1024, 11008, 8, 3), (512, 1024, 1, 1), (1024
     assert err <= 1e-5, (case, err)
 print('ok')
 """
-    env = dict(os.environ, BD_DELTA=mode.split("-")[0], BD_LUT_B1="1" if mode == "lut-b1" else "0")
+    env = dict(os.environ, BD_DELTA=mode)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
@@ -251,9 +251,9 @@ def test_multitenant_linear_permutation_bit_identical(cuda):
     assert torch.equal(Yp, Y[perm])
 
 
-@pytest.mark.parametrize("mode", ["mt4", "lut", "lut-b1", "fused", "units"])
+@pytest.mark.parametrize("mode", ["mt4", "lut", "units"])
 def test_multitenant_linear_each_delta_path(cuda, mode):
-    """Every K3 variant (byte-LUT, tensor-core fused, SIMT units) against the same f64 reference."""
+    """Every K3 variant (K23 FP4 tensor cores, byte-LUT, SIMT units) against the same f64 reference."""
     import subprocess
     import sys
 
@@ -278,7 +278,7 @@ for rows, cols, B, T in [(4096, 4096, 16, 16), (768, 11008, 8, 2), (1024, 2048, 
     assert err <= 1e-5, (rows, cols, B, T, err)
 print('ok')
 """
-    env = dict(os.environ, BD_DELTA=mode.split("-")[0], BD_LUT_B1="1" if mode == "lut-b1" else "0")
+    env = dict(os.environ, BD_DELTA=mode)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 

@@ -339,26 +339,6 @@ print('ok')
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
-def test_mxd_pool_one_request_per_tenant(cuda, port):
-    """K3t (deltas alone on the FP4 tensor cores beside K2, opt-in BD_MXD=1) in the pool:
-    one request per tenant on a 128-multiple shape, logits against the port."""
-    import subprocess
-    import sys
-
-    code = f"""
-import sys; sys.path.insert(0, {repr(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))})
-sys.path.insert(0, {repr(os.path.dirname(os.path.abspath(__file__)))})
-import oracle
-from test_gpu_pool import _k23_pool_run
-err = _k23_pool_run(oracle.port(), 1, 4)
-assert err <= 1e-2, err
-print('ok')
-"""
-    env = dict(os.environ, BD_MXD="1")
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
-
-
 def test_k23_pool_two_request_slots_short_plane_ring(cuda, port):
     """K23 with 2-request slots on one Llama-2-7B-shaped layer (8 tenants x 2 requests): the
     plane-stage ring is then as short as the producer count, the case whose mbarrier phases
