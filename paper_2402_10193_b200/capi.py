@@ -63,7 +63,7 @@ SYMBOLS = [
     "bd_compress", "bd_compress_batched", "bd_compress_stack", "bd_packed_signed_accumulate",
     "bd_packed_matvec", "bd_multitenant_linear", "bd_multitenant_linear_f32", "bd_pool_create", "bd_pool_destroy",
     "bd_pool_set_tensor", "bd_pool_register_delta", "bd_pool_register_delta_file",
-    "bd_pool_open_request", "bd_pool_close_request", "bd_pool_decode_step",
+    "bd_bdelta_validate", "bd_pool_open_request", "bd_pool_close_request", "bd_pool_decode_step",
     "bd_pool_decode_layers", "bd_pool_get_stats", "bd_pool_profile_layers", "bd_pool_profile_layers_serial", "bd_nccl_unique_id",
     "bd_pool_init_comm", "bd_pool_init_loopback", "bd_trace_enable", "bd_trace_read",
 ]
@@ -102,6 +102,7 @@ def lib() -> C.CDLL:
     L.bd_pool_profile_layers.argtypes = [vp, C.POINTER(Request), u64, vp, vp, C.POINTER(C.c_double),
                                          C.POINTER(u64), vp]
     L.bd_pool_profile_layers_serial.argtypes = L.bd_pool_profile_layers.argtypes
+    L.bd_bdelta_validate.argtypes = [C.c_char_p, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]
     L.bd_nccl_unique_id.argtypes = [vp]
     L.bd_pool_init_comm.argtypes = [vp, vp]
     L.bd_pool_init_loopback.argtypes = [vp, C.c_char_p]

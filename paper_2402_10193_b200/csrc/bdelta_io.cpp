@@ -10,6 +10,7 @@
 // trailing bits -> bad_argument.
 #include "bdelta_io.h"
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -87,7 +88,57 @@ struct JParser {
                     ++p;
                     if (p >= end) bad();
                     const char c = *p;
-                    v.str.push_back(c == 'n' ? '\n' : c == 't' ? '\t' : c);
+                    switch (c) {
+                        case '"': case '\\': case '/': v.str.push_back(c); break;
+                        case 'b': v.str.push_back('\b'); break;
+                        case 'f': v.str.push_back('\f'); break;
+                        case 'n': v.str.push_back('\n'); break;
+                        case 'r': v.str.push_back('\r'); break;
+                        case 't': v.str.push_back('\t'); break;
+                        case 'u': {  // \uXXXX (with surrogate pairs) -> UTF-8, as nlohmann::json
+                            auto hex4 = [&](const char* q) {
+                                if (end - q < 4) bad();
+                                uint32_t cp = 0;
+                                for (int i = 0; i < 4; ++i) {
+                                    const char h = q[i];
+                                    cp <<= 4;
+                                    if (h >= '0' && h <= '9') cp |= uint32_t(h - '0');
+                                    else if (h >= 'a' && h <= 'f') cp |= uint32_t(h - 'a' + 10);
+                                    else if (h >= 'A' && h <= 'F') cp |= uint32_t(h - 'A' + 10);
+                                    else bad();
+                                }
+                                return cp;
+                            };
+                            uint32_t cp = hex4(p + 1);
+                            p += 4;
+                            if (cp >= 0xD800 && cp < 0xDC00) {  // high surrogate: a low one must follow
+                                if (end - p < 7 || p[1] != '\\' || p[2] != 'u') bad();
+                                const uint32_t lo = hex4(p + 3);
+                                if (lo < 0xDC00 || lo >= 0xE000) bad();
+                                cp = 0x10000 + ((cp - 0xD800) << 10) + (lo - 0xDC00);
+                                p += 6;
+                            } else if (cp >= 0xDC00 && cp < 0xE000) {
+                                bad();
+                            }
+                            if (cp < 0x80) {
+                                v.str.push_back(char(cp));
+                            } else if (cp < 0x800) {
+                                v.str.push_back(char(0xC0 | (cp >> 6)));
+                                v.str.push_back(char(0x80 | (cp & 0x3F)));
+                            } else if (cp < 0x10000) {
+                                v.str.push_back(char(0xE0 | (cp >> 12)));
+                                v.str.push_back(char(0x80 | ((cp >> 6) & 0x3F)));
+                                v.str.push_back(char(0x80 | (cp & 0x3F)));
+                            } else {
+                                v.str.push_back(char(0xF0 | (cp >> 18)));
+                                v.str.push_back(char(0x80 | ((cp >> 12) & 0x3F)));
+                                v.str.push_back(char(0x80 | ((cp >> 6) & 0x3F)));
+                                v.str.push_back(char(0x80 | (cp & 0x3F)));
+                            }
+                            break;
+                        }
+                        default: bad();
+                    }
                 } else {
                     v.str.push_back(*p);
                 }
@@ -122,7 +173,9 @@ const JVal& field(const JVal& e, const char* k, const std::string& name) {
     return *v;
 }
 uint64_t as_u64(const JVal& v, const std::string& name) {
-    if (v.kind != JVal::Num || v.num < 0) fail(BD_ERR_JSON_PARSE, "tensor '" + name + "': bad number");
+    // whole, non-negative, exactly representable (nlohmann's get<uint64_t> on a JSON integer)
+    if (v.kind != JVal::Num || v.num < 0 || v.num != std::floor(v.num) || v.num > 9007199254740992.0)
+        fail(BD_ERR_JSON_PARSE, "tensor '" + name + "': bad number");
     return static_cast<uint64_t>(v.num);
 }
 
@@ -140,6 +193,8 @@ DeltaFileHost read_bdelta(const std::string& path) {
     JParser jp{reinterpret_cast<const char*>(bytes.data() + 12),
                reinterpret_cast<const char*>(bytes.data() + 12 + hlen)};
     const JVal header = jp.parse();
+    jp.ws();
+    require(jp.p == jp.end, BD_ERR_JSON_PARSE, path + ": trailing bytes after the JSON header");
     require(header.kind == JVal::Arr, BD_ERR_JSON_PARSE, path + ": header is not a JSON array");
     const uint8_t* payload = bytes.data() + 12 + hlen;
     const size_t payload_len = bytes.size() - 12 - hlen;

@@ -11,6 +11,7 @@
 #include <set>
 #include <vector>
 
+#include "bdelta_io.h"
 #include "common.cuh"
 #include "kernels.h"
 
@@ -412,6 +413,21 @@ int bd_pool_init_comm(bd_pool* pool, const void* id) {
     return guarded([&] {
         require(pool && id, BD_ERR_BAD_ARGUMENT, "init_comm: null argument");
         pool_init_comm(pool, id);
+    });
+}
+
+int bd_bdelta_validate(const char* path, uint64_t* n_tensors, uint64_t* n_packed, uint64_t* max_planes) {
+    return guarded([&] {
+        require(path != nullptr, BD_ERR_BAD_ARGUMENT, "bdelta_validate: null path");
+        const DeltaFileHost f = read_bdelta(path);
+        uint64_t packed = 0, mp = 0;
+        for (const auto& e : f.entries) {
+            packed += e.packed ? 1 : 0;
+            mp = std::max(mp, e.planes);
+        }
+        if (n_tensors) *n_tensors = f.entries.size();
+        if (n_packed) *n_packed = packed;
+        if (max_planes) *max_planes = mp;
     });
 }
 

@@ -81,3 +81,58 @@ def test_tensor_shapes_match_reference_order():
     if oracle.have_ref():
         cfg = json.dumps(dict(arch, rope_theta=10000.0))
         assert [tuple(t) for t in oracle.ref().tensor_specs(cfg)] == mine
+
+
+def _validate(path):
+    from paper_2402_10193_b200 import capi
+
+    n, k, mp = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    rc = capi.lib().bd_bdelta_validate(str(path).encode(), C.byref(n), C.byref(k), C.byref(mp))
+    return rc, n.value, k.value, mp.value
+
+
+def test_bdelta_reader_accepts_reference_files():
+    """Files written by the reference's write_delta_file (tests/golden) parse on the host:
+    the toy universe (1 plane) and the 2/3-plane universe."""
+    from conftest import GOLDEN
+
+    rc, n, k, mp = _validate(os.path.join(GOLDEN, "toy_t0.bdelta"))
+    assert rc == 0 and n == 21 and k == 14 and mp == 1
+    rc, n, k, mp = _validate(os.path.join(GOLDEN, "mp_t1.bdelta"))
+    assert rc == 0 and k == 7 and mp == 3
+
+
+def _rewrite_header(src, dst, transform):
+    import struct
+
+    b = open(src, "rb").read()
+    hlen = struct.unpack("<I", b[8:12])[0]
+    header = transform(b[12:12 + hlen])
+    open(dst, "wb").write(b[:8] + struct.pack("<I", len(header)) + header + b[12 + hlen:])
+
+
+def test_bdelta_reader_rejects_like_read_delta_file(tmp_path):
+    """read_delta_file (nlohmann) semantics: trailing bytes after the JSON array, fractional
+    sizes and bad escapes are json_parse errors; \\uXXXX escapes decode."""
+    import json
+
+    from conftest import GOLDEN
+
+    src = os.path.join(GOLDEN, "toy_t0.bdelta")
+    p = tmp_path / "x.bdelta"
+    _rewrite_header(src, p, lambda h: h + b" ]")
+    assert _validate(p)[0] == 3  # json_parse
+    _rewrite_header(src, p, lambda h: h.replace(b'"rows":1,', b'"rows":1.5,', 1))
+    assert _validate(p)[0] == 3
+    _rewrite_header(src, p, lambda h: h.replace(b'"embed"', b'"emb\\q"', 1))
+    assert _validate(p)[0] == 3
+
+    def rename(h):  # "embed" spelled with \u escapes: same name, parses
+        j = json.loads(h)
+        s = json.dumps(j).replace('"embed"', '"\\u0065mbed"', 1)
+        return s.encode()
+
+    _rewrite_header(src, p, rename)
+    assert _validate(p)[0] == 0
+    open(p, "wb").write(b"BDLT\x02\x00\x00\x00\x00\x00\x00\x00")
+    assert _validate(p)[0] == 2  # malformed_header (version)
