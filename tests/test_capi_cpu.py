@@ -136,3 +136,15 @@ def test_bdelta_reader_rejects_like_read_delta_file(tmp_path):
     assert _validate(p)[0] == 0
     open(p, "wb").write(b"BDLT\x02\x00\x00\x00\x00\x00\x00\x00")
     assert _validate(p)[0] == 2  # malformed_header (version)
+
+
+def test_doctest_shim_runs_reference_suites_on_the_reference():
+    """Control for tests/test_gpu_reference_suites.py: the same unchanged reference suites
+    through the doctest shim against the unmodified reference library (no GPU) all pass."""
+    import subprocess
+
+    exe = os.path.join(ROOT, "integration", "_build", "deltakit_tests_ref")
+    if not os.path.exists(exe):
+        pytest.skip("integration/_build not built (reference sources absent)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "[doctest] test cases: 39 passed, 0 failed, 0 skipped" in r.stdout, r.stdout[-3000:]
