@@ -20,6 +20,7 @@
 // consumer sums the slices in a fixed order (deterministic).
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -41,6 +42,7 @@ constexpr int kLutThreads = BD_LUT_THREADS;
 constexpr int kLutRegs = BD_LUT_REGS;
 constexpr int kSliceCols = 1024;
 constexpr size_t kTableBytes = 4 * 256 * 32 * sizeof(float);  // 128 KB
+constexpr size_t kLut2Smem = kTableBytes + (kSliceCols + kSliceCols / 128) * sizeof(float);
 constexpr int R = 16;                                          // rows per warp batch
 
 // Table layout (bytes): entry (k, e, lane l) at (k>>1)*65536 + e*256 + (k&1)*128 + 4*l,
@@ -203,6 +205,17 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     return d;
 }
 
+// lut2 keeps no static shared memory, so its dynamic buffer (tables first) starts right after
+// the CTA's 1 KB reserved shared memory: the table base is an immediate of every lookup
+// (checked at kernel entry)
+constexpr uint32_t kTableShared = 0x400;
+template <uint32_t kOff>
+__device__ __forceinline__ float lds_imm(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(addr), "n"(kOff));
+    return v;
+}
+
 __device__ __forceinline__ void build_tables_v2(float* T, const float* xs) {
     // thread t -> bank t & 31 (c = bank >> 2, b' = bank & 3), word w = (t >> 5) & 3,
     // quarter (t >> 7) of the 256 entries; a warp stores one 128-byte row per entry.
@@ -238,8 +251,8 @@ template <int kWPR>  // words per plane row (cols/32); 0 = runtime value
 __global__ void __maxnreg__(kLutRegs)
     lut2_kernel(const __grid_constant__ LutParams p, const uint16_t* __restrict__ X,
                 float* __restrict__ out) {
-    extern __shared__ float T[];
-    __shared__ float xs[kSliceCols + kSliceCols / 128];  // x of the slice, padded every 128
+    extern __shared__ float T[];   // [128 KB tables][x of the slice, padded every 128]
+    float* xs = T + kTableBytes / 4;
     const unsigned long long t_entry = gtimer();
     griddep_wait();  // PDL: X comes from the previous kernel; D is still read by it
     const unsigned long long t_wait = gtimer();
@@ -256,7 +269,7 @@ __global__ void __maxnreg__(kLutRegs)
         L |= (16u * chunk + 4u * bp) << (8 * b);
         sel[b] = 0xCC00u | (bp << 4) | (4u + b);
     }
-    const char* Tc = reinterpret_cast<const char*>(T);
+    if (threadIdx.x == 0 && static_cast<uint32_t>(__cvta_generic_to_shared(T)) != kTableShared) __trap();
     const int wpr = kWPR ? kWPR : p.cols / 32;
     const long long total = static_cast<long long>(p.n_jobs) * p.slices * p.M;
     const long long g0 = total * blockIdx.x / gridDim.x;
@@ -287,43 +300,39 @@ __global__ void __maxnreg__(kLutRegs)
             if (la >= lb) continue;
             const int n_planes = job.n_planes[s];
             for (int pl = 0; pl < n_planes; ++pl) {
-                const uint4* plane = reinterpret_cast<const uint4*>(job.bits[s][pl]) + slice * 8 + chunk;
+                // lanes past the matrix's last column read chunk 0 (their table entries are 0)
+                const uint4* plane = reinterpret_cast<const uint4*>(job.bits[s][pl]) + slice * 8 +
+                                     (lane_on ? chunk : 0);
                 const float a = job.alpha[s][pl];
-                // lane rows: r0 + 4 grp + i, i < 4 (each LDG.128 instruction: 4 rows x 128 B)
+                // lane rows r0 + 4 grp + i, i < 4 (each LDG.128 instruction: 4 rows x 128 B); rows
+                // past lb re-read row lb - 1 (never stored), so no load is predicated
                 auto load = [&](int r0, uint4 (&w)[4]) {
-                    const int rl = r0 + 4 * grp;
-                    const uint4* rowp = plane + static_cast<size_t>(rl) * (wpr / 4);
-                    if (lane_on && r0 + kRows <= lb) {
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) w[i] = __ldcs(rowp + i * (wpr / 4));
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            w[i] = (lane_on && rl + i < lb) ? __ldcs(rowp + i * (wpr / 4)) : make_uint4(0, 0, 0, 0);
+                    for (int i = 0; i < 4; ++i) {
+                        const int r = min(r0 + 4 * grp + i, lb - 1);
+                        w[i] = __ldcs(plane + static_cast<size_t>(r) * (wpr / 4));
                     }
                 };
-                uint4 wn[4];
-                int r0 = la + warp * kRows;
-                if (r0 < lb) load(r0, wn);
-                for (; r0 < lb; r0 += kWarps * kRows) {
-                    uint4 wc[4];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) wc[i] = wn[i];
-                    if (r0 + kWarps * kRows < lb) load(r0 + kWarps * kRows, wn);
+                auto consume = [&](int r0, const uint4 (&wc)[4]) {
                     float acc[4];
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         const uint32_t v[4] = {wc[i].x, wc[i].y, wc[i].z, wc[i].w};
                         float sw[4];
 #pragma unroll
-                        for (int w = 0; w < 4; ++w) {
-                            const char* Tw = Tc + 65536 * (w >> 1) + 128 * (w & 1);
-                            const float t0 = *reinterpret_cast<const float*>(Tw + prmt(v[w], L, sel[0]));
-                            const float t1 = *reinterpret_cast<const float*>(Tw + prmt(v[w], L, sel[1]));
-                            const float t2 = *reinterpret_cast<const float*>(Tw + prmt(v[w], L, sel[2]));
-                            const float t3 = *reinterpret_cast<const float*>(Tw + prmt(v[w], L, sel[3]));
-                            sw[w] = (t0 + t1) + (t2 + t3);
-                        }
+                        // every lookup is one PRMT + one LDS [reg + imm]
+                        auto word = [&](uint32_t vw, auto off) {
+                            constexpr uint32_t o = decltype(off)::value;
+                            const float t0 = lds_imm<o>(prmt(vw, L, sel[0]));
+                            const float t1 = lds_imm<o>(prmt(vw, L, sel[1]));
+                            const float t2 = lds_imm<o>(prmt(vw, L, sel[2]));
+                            const float t3 = lds_imm<o>(prmt(vw, L, sel[3]));
+                            return (t0 + t1) + (t2 + t3);
+                        };
+                        sw[0] = word(v[0], std::integral_constant<uint32_t, kTableShared>{});
+                        sw[1] = word(v[1], std::integral_constant<uint32_t, kTableShared + 128>{});
+                        sw[2] = word(v[2], std::integral_constant<uint32_t, kTableShared + 65536>{});
+                        sw[3] = word(v[3], std::integral_constant<uint32_t, kTableShared + 65536 + 128>{});
                         acc[i] = a * ((sw[0] + sw[1]) + (sw[2] + sw[3]));
                     }
                     // transposing butterfly over the chunk bits (lane bits 2, 1), then a pair sum:
@@ -344,6 +353,21 @@ __global__ void __maxnreg__(kLutRegs)
                         if (pl == 0) out_u[s0 + r] = tot;
                         else out_u[s0 + r] += tot;  // same thread wrote it for plane 0
                     }
+                };
+                // ping-pong register buffers: the next batch's words are in flight while the
+                // current one is looked up (no register moves between iterations)
+                constexpr int kStep = kWarps * kRows;
+                uint4 wa[4], wb[4];
+                int r0 = la + warp * kRows;
+                if (r0 < lb) load(r0, wa);
+                while (r0 < lb) {
+                    if (r0 + kStep < lb) load(r0 + kStep, wb);
+                    consume(r0, wa);
+                    r0 += kStep;
+                    if (r0 >= lb) break;
+                    if (r0 + kStep < lb) load(r0 + kStep, wa);
+                    consume(r0, wb);
+                    r0 += kStep;
                 }
             }
         }
@@ -408,7 +432,7 @@ void lut2_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t s
     static bool attr = false;
     if (!attr) {
         BD_CUDA(cudaFuncSetAttribute(lut2_kernel<kWPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(kTableBytes)));
+                                     int(kLut2Smem)));
         // max carveout (K2 co-resident on every SM) where plane rows are 128-B aligned; the
         // down projection (1376-B rows) measured faster on the default carveout, K2 after
         // it (profiles/r02_exp_down_carveout.txt: 1.487 vs 1.857 ms/step for down)
@@ -417,7 +441,7 @@ void lut2_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t s
                                          int(cudaSharedmemCarveoutMaxShared)));
         attr = true;
     }
-    BD_CUDA(launch_pdl(lut2_kernel<kWPR>, dim3(p.grid), dim3(kLutThreads), kTableBytes, stream, p,
+    BD_CUDA(launch_pdl(lut2_kernel<kWPR>, dim3(p.grid), dim3(kLutThreads), kLut2Smem, stream, p,
                        static_cast<const uint16_t*>(X), out));
 }
 
