@@ -110,6 +110,25 @@ int bd_packed_signed_accumulate(const uint8_t* bits, uint64_t rows, uint64_t col
 int bd_packed_matvec(const uint8_t* bits, float alpha, uint64_t rows, uint64_t cols,
                      const float* x, uint64_t n_vec, float* y, void* stream);
 
+/* ------------------------------------------------- K6: distill backward -- */
+/* Replaces deltakit::packed_signed_accumulate_t (P:include/deltakit/delta.hpp:71-72,
+ * P:src/delta.cpp:105-131) for n_vec vectors at once (accumulates, like the reference):
+ *   out[v*cols + j] += sum_i s_ij * y[v*rows + i],  s = +1 for bit 1, -1 for bit 0;
+ * column sums in fp64, rounded to f32 once. Any rows/cols. Device pointers. */
+int bd_packed_signed_accumulate_t(const uint8_t* bits, uint64_t rows, uint64_t cols, const float* y,
+                                  uint64_t n_vec, float* out, void* stream);
+/* The packed-plane part of the distillation backward: linear_backward's PackedDelta branch
+ * (P:src/model.cpp:87-107) for one linear with n_planes sign planes of [rows x cols]:
+ *   dx[t*cols + j] += scales[pl] * float((S_pl^T dy[t])[j])     t < s (accumulated)
+ *   scale_grad[pl] += sum_i double(dy[i]) * double(plane_u[pl][i])  (i < s*rows, accumulated)
+ * dy: device f32 [s x rows]; plane_u[pl]: device f32 [s x rows], the forward's S_pl x
+ * (LinearTape::plane_u); dx: device f32 [s x cols]; scale_grad: device f64 [n_planes].
+ * plane_bits / plane_u / scales are HOST arrays of n_planes entries. The branch's dense
+ * dy * W_base term is a plain library GEMM (cuBLAS / torch.matmul), left to the caller. */
+int bd_delta_linear_backward(int32_t n_planes, const uint8_t* const* plane_bits, const float* scales,
+                             uint64_t rows, uint64_t cols, const float* dy, uint64_t s,
+                             const float* const* plane_u, float* dx, double* scale_grad, void* stream);
+
 /* --------------------------------------------------------------- K2+K3 -- */
 /* One multi-tenant linear (the per-projection body of ServingPool::decode_shared,
  * P:src/serve.cpp:247-254: backbone_linear_nt serve.cpp:120-127 + per-request

@@ -9,6 +9,7 @@
 // integration/Makefile, so these win at link time):
 //   compress_delta, compress_tensor, compress_stack         delta.cpp:16-34, 57-70  -> K1
 //   packed_signed_accumulate, packed_matvec                 delta.cpp:72-103        -> K3 drop-in
+//   packed_signed_accumulate_t                              delta.cpp:105-131       -> K6 (distill backward)
 //   ServingPool::decode_shared, ServingPool::decode_naive   serve.cpp:205-342       -> device pool
 // The ServingPool forward runs in a device pool (bd_pool) created on first use for each
 // reference ServingPool object; tenants are uploaded from the reference's own DeltaFile
@@ -117,6 +118,16 @@ void packed_signed_accumulate(const PackedSignMatrix& p, std::span<const float> 
     Dev<uint8_t> bits(p.bits.data(), p.bits.size());
     Dev<float> dx(x.data(), x.size()), dout(out.data(), out.size());
     ok(bd_packed_signed_accumulate(bits.p, p.rows, p.cols, dx.p, 1, dout.p, nullptr));
+    dout.to_host(out.data(), out.size());
+}
+
+void packed_signed_accumulate_t(const PackedSignMatrix& p, std::span<const float> y, std::span<float> out) {
+    check(y.size() == p.rows && out.size() == p.cols, errc::length_mismatch,
+          "packed_signed_accumulate_t: length mismatch");
+    if (p.cols == 0) return;
+    Dev<uint8_t> bits(p.bits.data(), p.bits.size());
+    Dev<float> dy(y.data(), y.size()), dout(out.data(), out.size());
+    ok(bd_packed_signed_accumulate_t(bits.p, p.rows, p.cols, dy.p, 1, dout.p, nullptr));
     dout.to_host(out.data(), out.size());
 }
 

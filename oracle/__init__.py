@@ -131,6 +131,12 @@ class _Common:
         self._psa(np.ascontiguousarray(bits, np.uint8), rows, cols, x, out)
         return out
 
+    def packed_signed_accumulate_t(self, bits, rows: int, cols: int, y, out=None) -> np.ndarray:
+        y = _f32(y)
+        out = np.zeros(cols, np.float32) if out is None else _f32(out).copy()
+        self._psat(np.ascontiguousarray(bits, np.uint8), rows, cols, y, out)
+        return out
+
     def packed_matvec(self, bits, rows: int, cols: int, scale: float, x) -> np.ndarray:
         y = np.zeros(rows, np.float32)
         self._pmv(np.ascontiguousarray(bits, np.uint8), rows, cols, scale, _f32(x), y)
@@ -170,6 +176,9 @@ class Ref(_Common):
 
     def _psa(self, bits, rows, cols, x, out):
         self._chk(self.lib.dkref_packed_signed_accumulate(_p(bits, C.c_uint8), u64(rows), u64(cols), _p(x, C.c_float), _p(out, C.c_float)))
+
+    def _psat(self, bits, rows, cols, y, out):
+        self._chk(self.lib.dkref_packed_signed_accumulate_t(_p(bits, C.c_uint8), u64(rows), u64(cols), _p(y, C.c_float), _p(out, C.c_float)))
 
     def _pmv(self, bits, rows, cols, scale, x, y):
         self._chk(self.lib.dkref_packed_matvec(_p(bits, C.c_uint8), u64(rows), u64(cols), C.c_float(scale), _p(x, C.c_float), _p(y, C.c_float)))
@@ -287,6 +296,9 @@ class Port(_Common):
 
     def _psa(self, bits, rows, cols, x, out):
         self.lib.bdo_packed_signed_accumulate(_p(bits, C.c_uint8), u64(rows), u64(cols), _p(x, C.c_float), _p(out, C.c_float))
+
+    def _psat(self, bits, rows, cols, y, out):
+        self.lib.bdo_packed_signed_accumulate_t(_p(bits, C.c_uint8), u64(rows), u64(cols), _p(y, C.c_float), _p(out, C.c_float))
 
     def _pmv(self, bits, rows, cols, scale, x, y):
         self.lib.bdo_packed_matvec(_p(bits, C.c_uint8), u64(rows), u64(cols), C.c_float(scale), _p(x, C.c_float), _p(y, C.c_float))

@@ -83,6 +83,33 @@ void bdo_packed_signed_accumulate(const uint8_t* bits, uint64_t rows, uint64_t c
     }
 }
 
+/* P:src/delta.cpp:105-131: out[j] += float(2 * sum_{bit(i,j)=1} y_i - sum_i y_i), double sums,
+ * rows with y_i == 0 skipped (they add nothing) */
+void bdo_packed_signed_accumulate_t(const uint8_t* bits, uint64_t rows, uint64_t cols,
+                                    const float* y, float* out) {
+    double* acc = (double*)calloc(cols ? cols : 1, sizeof(double));
+    double total = 0.0;
+    for (uint64_t r = 0; r < rows; ++r) total += y[r];
+    for (uint64_t r = 0; r < rows; ++r) {
+        const double yr = y[r];
+        if (yr == 0.0) continue;
+        uint64_t idx = r * cols, c = 0;
+        while (c < cols) {
+            uint8_t byte = (uint8_t)(bits[idx >> 3] >> (idx & 7));
+            uint64_t take = 8 - (idx & 7);
+            if (take > cols - c) take = cols - c;
+            for (uint64_t b = 0; b < take; ++b) {
+                if (byte & 1u) acc[c + b] += yr;
+                byte >>= 1;
+            }
+            c += take;
+            idx += take;
+        }
+    }
+    for (uint64_t j = 0; j < cols; ++j) out[j] += (float)(2.0 * acc[j] - total);
+    free(acc);
+}
+
 /* delta.cpp:72-78 */
 void bdo_packed_matvec(const uint8_t* bits, uint64_t rows, uint64_t cols, float scale,
                        const float* x, float* y) {

@@ -27,6 +27,8 @@ void bdo_compress_stack(const float* base, const float* fine, uint64_t n, uint64
                         uint8_t* bits, float* scales);      /* delta.cpp:57-70 */
 void bdo_packed_signed_accumulate(const uint8_t* bits, uint64_t rows, uint64_t cols,
                                   const float* x, float* out); /* delta.cpp:80-103 */
+void bdo_packed_signed_accumulate_t(const uint8_t* bits, uint64_t rows, uint64_t cols,
+                                    const float* y, float* out);   /* delta.cpp:105-131 */
 void bdo_packed_matvec(const uint8_t* bits, uint64_t rows, uint64_t cols, float scale,
                        const float* x, float* y);           /* delta.cpp:72-78 */
 void bdo_matmul_nt(const float* a, uint64_t s, uint64_t k, const float* b, uint64_t t,

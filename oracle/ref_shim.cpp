@@ -132,6 +132,18 @@ int dkref_packed_signed_accumulate(const std::uint8_t* bits, std::uint64_t rows,
     });
 }
 
+// delta.cpp:105-131 (accumulates into out, like the reference)
+int dkref_packed_signed_accumulate_t(const std::uint8_t* bits, std::uint64_t rows,
+                                     std::uint64_t cols, const float* y, float* out) {
+    return guard([&] {
+        PackedSignMatrix p;
+        p.rows = rows;
+        p.cols = cols;
+        p.bits.assign(bits, bits + PackedSignMatrix::packed_size(rows, cols));
+        packed_signed_accumulate_t(p, {y, rows}, {out, cols});
+    });
+}
+
 // delta.cpp:72-78
 int dkref_packed_matvec(const std::uint8_t* bits, std::uint64_t rows, std::uint64_t cols,
                         float scale, const float* x, float* y) {

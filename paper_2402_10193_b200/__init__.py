@@ -155,6 +155,38 @@ def packed_matvec(bits, alpha: float, rows: int, cols: int, x, stream=None):
     return y
 
 
+def packed_signed_accumulate_t(bits, rows: int, cols: int, y, out, stream=None):
+    """packed_signed_accumulate_t (delta.hpp:71-72, delta.cpp:105-131): out += S^T y, for y of
+    shape [rows] or [n_vec, rows] (f32, device). Accumulates in place into `out`."""
+    _req_cuda(bits, y, out)
+    n_vec = 1 if y.dim() == 1 else y.shape[0]
+    if y.shape[-1] != rows or out.shape[-1] != cols or out.numel() != n_vec * cols:
+        raise BitDeltaError(8, "packed_signed_accumulate_t: length mismatch")
+    check(lib().bd_packed_signed_accumulate_t(_ptr(bits), rows, cols, _ptr(y.contiguous()), n_vec, _ptr(out),
+                                              _stream(stream)))
+    return out
+
+
+def delta_linear_backward(planes, scales, rows: int, cols: int, dy, plane_u, dx, scale_grad, stream=None):
+    """The packed-plane part of linear_backward's PackedDelta branch (model.cpp:87-107):
+    dx += sum_pl scales[pl] * (S_pl^T dy[t]) per row t of dy [s, rows]; scale_grad[pl] (f64,
+    device) += sum(dy * plane_u[pl]). The dense dy @ W_base term is the caller's GEMM."""
+    import ctypes as C
+
+    n = len(planes)
+    _req_cuda(dy, dx, scale_grad, *planes, *plane_u)
+    s = dy.shape[0] if dy.dim() > 1 else 1
+    if dy.shape[-1] != rows or dx.shape[-1] != cols or dx.numel() != s * cols or len(plane_u) != n \
+            or len(scales) != n or scale_grad.numel() < n or any(u.numel() != s * rows for u in plane_u):
+        raise BitDeltaError(8, "delta_linear_backward: length mismatch")
+    bits = (C.c_void_p * max(n, 1))(*[_ptr(b) for b in planes])
+    us = (C.c_void_p * max(n, 1))(*[_ptr(u.contiguous()) for u in plane_u])
+    sc = (C.c_float * max(n, 1))(*[float(a) for a in scales])
+    check(lib().bd_delta_linear_backward(n, bits, sc, rows, cols, _ptr(dy.contiguous()), s, us, _ptr(dx),
+                                         _ptr(scale_grad), _stream(stream)))
+    return dx, scale_grad
+
+
 def multitenant_linear(W, tenant_bits, tenant_alpha, req_tenant, X, stream=None):
     """Y[b] = X[b] W^T + alpha[t(b)] S_t(b) X[b]   (f32 Y).
 

@@ -360,6 +360,29 @@ int bd_packed_matvec(const uint8_t* bits, float alpha, uint64_t rows, uint64_t c
     });
 }
 
+int bd_packed_signed_accumulate_t(const uint8_t* bits, uint64_t rows, uint64_t cols, const float* y,
+                                  uint64_t n_vec, float* out, void* stream) {
+    return guarded([&] {
+        packed_transpose_launch(bits, rows, cols, y, n_vec, out, 1.0f, false, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int bd_delta_linear_backward(int32_t n_planes, const uint8_t* const* plane_bits, const float* scales,
+                             uint64_t rows, uint64_t cols, const float* dy, uint64_t s,
+                             const float* const* plane_u, float* dx, double* scale_grad, void* stream) {
+    return guarded([&] {
+        require(n_planes >= 0, BD_ERR_BAD_ARGUMENT, "delta_linear_backward: negative plane count");
+        require(n_planes == 0 || (plane_bits && scales && plane_u && scale_grad), BD_ERR_BAD_ARGUMENT,
+                "delta_linear_backward: null pointer");
+        require(dy && dx, BD_ERR_BAD_ARGUMENT, "delta_linear_backward: null pointer");
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        for (int32_t pl = 0; pl < n_planes; ++pl) {
+            dot_f64_launch(dy, plane_u[pl], s * rows, scale_grad + pl, st);
+            packed_transpose_launch(plane_bits[pl], rows, cols, dy, s, dx, scales[pl], false, st);
+        }
+    });
+}
+
 int bd_multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int32_t n_tenants,
                           const uint8_t* const* tenant_bits, const float* tenant_alpha,
                           int32_t batch, const int32_t* req_tenant, const void* X, float* Y,

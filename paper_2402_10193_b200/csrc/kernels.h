@@ -40,6 +40,13 @@ void packed_accumulate_launch(const uint8_t* bits, uint64_t rows, uint64_t cols,
                               uint64_t n_vec, float* out, float scale, bool overwrite,
                               cudaStream_t stream);
 
+// ---- K6 distill backward (backward.cu) ----
+// out[v][j] (overwrite ? = : +=) scale * float(sum_i s_ij y[v][i])  (P:src/delta.cpp:105-131)
+void packed_transpose_launch(const uint8_t* bits, uint64_t rows, uint64_t cols, const float* y,
+                             uint64_t n_vec, float* out, float scale, bool overwrite, cudaStream_t s);
+// acc[0] += sum_i double(a[i]) * double(b[i])  (P:src/model.cpp:92-95)
+void dot_f64_launch(const float* a, const float* b, uint64_t n, double* acc, cudaStream_t s);
+
 // ---- K3 multi-tenant delta ----
 // One delta "unit" = one sign plane of one tenant applied to the rows
 // [row0, row0+rows) of a (possibly stacked) projection output, for the

@@ -436,7 +436,11 @@ void lut2_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t s
         // max carveout (K2 co-resident on every SM) where plane rows are 128-B aligned; the
         // down projection (1376-B rows) measured faster on the default carveout, K2 after
         // it (profiles/r02_exp_down_carveout.txt: 1.487 vs 1.857 ms/step for down)
+#ifdef BD_LUT_CARVE_ALL
+        if (true)
+#else
         if (kWPR % 32 == 0 && kWPR > 0)
+#endif
             BD_CUDA(cudaFuncSetAttribute(lut2_kernel<kWPR>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          int(cudaSharedmemCarveoutMaxShared)));
         attr = true;
