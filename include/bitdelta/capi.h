@@ -110,6 +110,19 @@ int bd_packed_signed_accumulate(const uint8_t* bits, uint64_t rows, uint64_t col
 int bd_packed_matvec(const uint8_t* bits, float alpha, uint64_t rows, uint64_t cols,
                      const float* x, uint64_t n_vec, float* y, void* stream);
 
+/* ------------------------------------------------ K2 int8: RTN backbone -- */
+/* rtn_quantize (P:src/int8.cpp:15-42), bit-exact: per row s = amax/127 (f32), q = clamp(
+ * nearbyint(double(w)/double(s)), -127, 127); an all-zero row gets s = 0. W: device f32
+ * [rows x cols]; q: device int8 [rows x cols]; row_scales: device f32 [rows]. Fails with
+ * BD_ERR_NON_FINITE on NaN/inf entries (synchronises the stream to report it). */
+int bd_rtn_quantize(const float* W, uint64_t rows, uint64_t cols, int8_t* q, float* row_scales, void* stream);
+/* int8_matmul_nt (P:src/int8.cpp:67-81): Y[i][r] = (A[i] . q[r]) * row_scales[r], A device f32
+ * [s x in_dim], q device int8 [out_dim x in_dim], Y device f32 [s x out_dim] (overwritten).
+ * tcgen05 kind::i8 against 4 int8 pieces of each A row (exact s32 accumulation; A to 2^-27
+ * of its row maximum): within the reference's own f32 rounding (rel-L2 <= 1e-5). */
+int bd_int8_matmul_nt(const float* A, uint64_t s, uint64_t in_dim, const int8_t* q, const float* row_scales,
+                      uint64_t out_dim, float* Y, void* stream);
+
 /* ------------------------------------------------- K6: distill backward -- */
 /* Replaces deltakit::packed_signed_accumulate_t (P:include/deltakit/delta.hpp:71-72,
  * P:src/delta.cpp:105-131) for n_vec vectors at once (accumulates, like the reference):

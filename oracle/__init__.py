@@ -142,6 +142,21 @@ class _Common:
         self._pmv(np.ascontiguousarray(bits, np.uint8), rows, cols, scale, _f32(x), y)
         return y
 
+    def rtn_quantize(self, w):
+        w = _f32(w)
+        rows, cols = w.shape
+        q = np.zeros((rows, cols), np.int8)
+        sc = np.zeros(rows, np.float32)
+        self._rtn(w, rows, cols, q, sc)
+        return q, sc
+
+    def int8_matmul_nt(self, a, q, scales) -> np.ndarray:
+        a = _f32(a)
+        q = np.ascontiguousarray(q, np.int8)
+        out = np.zeros((a.shape[0], q.shape[0]), np.float32)
+        self._i8mm(a, a.shape[0], q, _f32(scales), q.shape[0], q.shape[1], out)
+        return out
+
     def matmul_nt(self, a, b) -> np.ndarray:
         a, b = _f32(a), _f32(b)
         out = np.zeros((a.shape[0], b.shape[0]), np.float32)
@@ -176,6 +191,12 @@ class Ref(_Common):
 
     def _psa(self, bits, rows, cols, x, out):
         self._chk(self.lib.dkref_packed_signed_accumulate(_p(bits, C.c_uint8), u64(rows), u64(cols), _p(x, C.c_float), _p(out, C.c_float)))
+
+    def _rtn(self, w, rows, cols, q, sc):
+        self._chk(self.lib.dkref_rtn_quantize(_p(w, C.c_float), u64(rows), u64(cols), _p(q, C.c_int8), _p(sc, C.c_float)))
+
+    def _i8mm(self, a, s, q, sc, rows, cols, out):
+        self._chk(self.lib.dkref_int8_matmul_nt(_p(a, C.c_float), u64(s), _p(q, C.c_int8), _p(sc, C.c_float), u64(rows), u64(cols), _p(out, C.c_float)))
 
     def _psat(self, bits, rows, cols, y, out):
         self._chk(self.lib.dkref_packed_signed_accumulate_t(_p(bits, C.c_uint8), u64(rows), u64(cols), _p(y, C.c_float), _p(out, C.c_float)))
@@ -296,6 +317,12 @@ class Port(_Common):
 
     def _psa(self, bits, rows, cols, x, out):
         self.lib.bdo_packed_signed_accumulate(_p(bits, C.c_uint8), u64(rows), u64(cols), _p(x, C.c_float), _p(out, C.c_float))
+
+    def _rtn(self, w, rows, cols, q, sc):
+        self.lib.bdo_rtn_quantize(_p(w, C.c_float), u64(rows), u64(cols), _p(q, C.c_int8), _p(sc, C.c_float))
+
+    def _i8mm(self, a, s, q, sc, rows, cols, out):
+        self.lib.bdo_int8_matmul_nt(_p(a, C.c_float), u64(s), _p(q, C.c_int8), _p(sc, C.c_float), u64(rows), u64(cols), _p(out, C.c_float))
 
     def _psat(self, bits, rows, cols, y, out):
         self.lib.bdo_packed_signed_accumulate_t(_p(bits, C.c_uint8), u64(rows), u64(cols), _p(y, C.c_float), _p(out, C.c_float))

@@ -110,6 +110,37 @@ void bdo_packed_signed_accumulate_t(const uint8_t* bits, uint64_t rows, uint64_t
     free(acc);
 }
 
+/* P:src/int8.cpp:15-42: per row s = amax / 127 (f32); a zero row -> s = 0, q = 0; else
+ * q = clamp(nearbyint(double(w) / double(s)), -127, 127) (ties to even) */
+void bdo_rtn_quantize(const float* w, uint64_t rows, uint64_t cols, int8_t* q, float* scales) {
+    for (uint64_t r = 0; r < rows; ++r) {
+        const float* row = w + r * cols;
+        float amax = 0.0f;
+        for (uint64_t c = 0; c < cols; ++c) amax = fmaxf(amax, fabsf(row[c]));
+        const float s = amax / 127.0f;
+        scales[r] = s;
+        for (uint64_t c = 0; c < cols; ++c) {
+            double v = 0.0;
+            if (s != 0.0f) {
+                v = nearbyint((double)row[c] / (double)s);
+                v = v < -127.0 ? -127.0 : (v > 127.0 ? 127.0 : v);
+            }
+            q[r * cols + c] = (int8_t)v;
+        }
+    }
+}
+
+/* P:src/int8.cpp:67-81: out[i][r] = (sequential f32 sum of float(q) * a) * s_r */
+void bdo_int8_matmul_nt(const float* a, uint64_t s, const int8_t* q, const float* scales,
+                        uint64_t rows, uint64_t cols, float* out) {
+    for (uint64_t i = 0; i < s; ++i)
+        for (uint64_t r = 0; r < rows; ++r) {
+            float acc = 0.0f;
+            for (uint64_t c = 0; c < cols; ++c) acc += (float)q[r * cols + c] * a[i * cols + c];
+            out[i * rows + r] = acc * scales[r];
+        }
+}
+
 /* delta.cpp:72-78 */
 void bdo_packed_matvec(const uint8_t* bits, uint64_t rows, uint64_t cols, float scale,
                        const float* x, float* y) {

@@ -29,6 +29,10 @@ void bdo_packed_signed_accumulate(const uint8_t* bits, uint64_t rows, uint64_t c
                                   const float* x, float* out); /* delta.cpp:80-103 */
 void bdo_packed_signed_accumulate_t(const uint8_t* bits, uint64_t rows, uint64_t cols,
                                     const float* y, float* out);   /* delta.cpp:105-131 */
+void bdo_rtn_quantize(const float* w, uint64_t rows, uint64_t cols, int8_t* q,
+                      float* scales);                                   /* P:src/int8.cpp:15-42 */
+void bdo_int8_matmul_nt(const float* a, uint64_t s, const int8_t* q, const float* scales,
+                        uint64_t rows, uint64_t cols, float* out);      /* int8.cpp:67-81 */
 void bdo_packed_matvec(const uint8_t* bits, uint64_t rows, uint64_t cols, float scale,
                        const float* x, float* y);           /* delta.cpp:72-78 */
 void bdo_matmul_nt(const float* a, uint64_t s, uint64_t k, const float* b, uint64_t t,

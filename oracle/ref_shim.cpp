@@ -24,6 +24,7 @@
 #include "deltakit/arch.hpp"
 #include "deltakit/checkpoint.hpp"
 #include "deltakit/delta.hpp"
+#include "deltakit/int8.hpp"
 #include "deltakit/error.hpp"
 #include "deltakit/matrix.hpp"
 #include "deltakit/nn_ops.hpp"
@@ -141,6 +142,30 @@ int dkref_packed_signed_accumulate_t(const std::uint8_t* bits, std::uint64_t row
         p.cols = cols;
         p.bits.assign(bits, bits + PackedSignMatrix::packed_size(rows, cols));
         packed_signed_accumulate_t(p, {y, rows}, {out, cols});
+    });
+}
+
+// int8.cpp:15-42
+int dkref_rtn_quantize(const float* w, std::uint64_t rows, std::uint64_t cols, std::int8_t* q,
+                       float* scales) {
+    return guard([&] {
+        const Int8Tensor t = rtn_quantize(DenseMatrix(rows, cols, std::vector<float>(w, w + rows * cols)));
+        std::memcpy(q, t.values.data(), t.values.size());
+        std::memcpy(scales, t.row_scales.data(), rows * sizeof(float));
+    });
+}
+
+// int8.cpp:67-81: out (s x rows) = a (s x cols) * q^T, row scale applied after the f32 sum
+int dkref_int8_matmul_nt(const float* a, std::uint64_t s, const std::int8_t* q, const float* scales,
+                         std::uint64_t rows, std::uint64_t cols, float* out) {
+    return guard([&] {
+        Int8Tensor t;
+        t.rows = rows;
+        t.cols = cols;
+        t.values.assign(q, q + rows * cols);
+        t.row_scales.assign(scales, scales + rows);
+        const DenseMatrix y = int8_matmul_nt(DenseMatrix(s, cols, std::vector<float>(a, a + s * cols)), t);
+        std::memcpy(out, y.values().data(), s * rows * sizeof(float));
     });
 }
 

@@ -187,6 +187,37 @@ def delta_linear_backward(planes, scales, rows: int, cols: int, dy, plane_u, dx,
     return dx, scale_grad
 
 
+def rtn_quantize(W, stream=None):
+    """rtn_quantize (int8.hpp, int8.cpp:15-42): int8 [rows, cols] values and f32 row scales,
+    bit-exact with the reference. W: f32 [rows, cols] on the device."""
+    import torch
+
+    _req_cuda(W)
+    w = W.contiguous()
+    if w.dtype != torch.float32 or w.dim() != 2:
+        raise BitDeltaError(5, "rtn_quantize: expects a 2-D f32 tensor")
+    q = torch.empty(w.shape, dtype=torch.int8, device=w.device)
+    sc = torch.empty(w.shape[0], dtype=torch.float32, device=w.device)
+    check(lib().bd_rtn_quantize(_ptr(w), w.shape[0], w.shape[1], _ptr(q), _ptr(sc), _stream(stream)))
+    return q, sc
+
+
+def int8_matmul_nt(A, q, row_scales, stream=None):
+    """int8_matmul_nt (int8.cpp:67-81): A [s, in] f32 times the int8 RTN tensor q [out, in]
+    (row scales applied after the sum) -> [s, out] f32, on the tensor cores (kind::i8)."""
+    import torch
+
+    _req_cuda(A, q, row_scales)
+    a = A.contiguous()
+    if a.shape[-1] != q.shape[1] or row_scales.numel() != q.shape[0]:
+        raise BitDeltaError(6, "int8_matmul_nt: inner dimensions differ")
+    s = 1 if a.dim() == 1 else a.shape[0]
+    y = torch.empty((s, q.shape[0]) if a.dim() > 1 else (q.shape[0],), dtype=torch.float32, device=a.device)
+    check(lib().bd_int8_matmul_nt(_ptr(a), s, q.shape[1], _ptr(q.contiguous()), _ptr(row_scales.contiguous()),
+                                  q.shape[0], _ptr(y), _stream(stream)))
+    return y
+
+
 def multitenant_linear(W, tenant_bits, tenant_alpha, req_tenant, X, stream=None):
     """Y[b] = X[b] W^T + alpha[t(b)] S_t(b) X[b]   (f32 Y).
 

@@ -61,7 +61,7 @@ class PoolStats(C.Structure):
 SYMBOLS = [
     "bd_abi_version", "bd_last_error", "bd_device_check", "bd_launch_count", "bd_packed_size",
     "bd_compress", "bd_compress_batched", "bd_compress_stack", "bd_packed_signed_accumulate",
-    "bd_packed_matvec", "bd_packed_signed_accumulate_t", "bd_delta_linear_backward", "bd_multitenant_linear", "bd_multitenant_linear_f32", "bd_pool_create", "bd_pool_destroy",
+    "bd_packed_matvec", "bd_packed_signed_accumulate_t", "bd_delta_linear_backward", "bd_rtn_quantize", "bd_int8_matmul_nt", "bd_multitenant_linear", "bd_multitenant_linear_f32", "bd_pool_create", "bd_pool_destroy",
     "bd_pool_set_tensor", "bd_pool_register_delta", "bd_pool_register_delta_file",
     "bd_bdelta_validate", "bd_pool_open_request", "bd_pool_close_request", "bd_pool_decode_step",
     "bd_pool_decode_layers", "bd_pool_get_stats", "bd_pool_profile_layers", "bd_pool_profile_layers_serial", "bd_nccl_unique_id",
@@ -86,6 +86,8 @@ def lib() -> C.CDLL:
     L.bd_packed_signed_accumulate.argtypes = [vp, u64, u64, vp, u64, vp, vp]
     L.bd_packed_matvec.argtypes = [vp, C.c_float, u64, u64, vp, u64, vp, vp]
     L.bd_packed_signed_accumulate_t.argtypes = [vp, u64, u64, vp, u64, vp, vp]
+    L.bd_rtn_quantize.argtypes = [vp, u64, u64, vp, vp, vp]
+    L.bd_int8_matmul_nt.argtypes = [vp, u64, u64, vp, vp, u64, vp, vp]
     L.bd_delta_linear_backward.argtypes = [C.c_int32, C.POINTER(vp), C.POINTER(C.c_float), u64, u64, vp, u64,
                                            C.POINTER(vp), vp, vp, vp]
     L.bd_multitenant_linear.argtypes = [vp, u64, u64, C.c_int32, C.POINTER(vp), C.POINTER(C.c_float),

@@ -262,6 +262,49 @@ void multitenant_linear(const void* W, uint64_t out_dim, uint64_t in_dim, int32_
     BD_CUDA(cudaFreeAsync(D, stream));
 }
 
+// int8_matmul_nt (P:src/int8.cpp:67-81) on the tensor cores: Y [s x out] = A Wq^T * row_scale
+static void int8_matmul_impl(const float* A, uint64_t s, uint64_t in_dim, const int8_t* q,
+                             const float* row_scales, uint64_t out_dim, float* Y, cudaStream_t stream) {
+    require(A && q && row_scales && Y, BD_ERR_BAD_ARGUMENT, "int8_matmul_nt: null pointer");
+    if (s == 0 || out_dim == 0) return;
+    if (in_dim == 0) {
+        BD_CUDA(cudaMemsetAsync(Y, 0, s * out_dim * sizeof(float), stream));
+        return;
+    }
+    require(out_dim <= 0x7fffffffull && in_dim <= 0x7fffffffull, BD_ERR_BAD_ARGUMENT, "int8_matmul_nt: too large");
+    // TMA needs 16-byte row strides: copy Wq into a padded buffer when in_dim % 16 != 0
+    const uint64_t ld = (in_dim + 15) / 16 * 16;
+    int8_t* wq = const_cast<int8_t*>(q);
+    int8_t* wpad = nullptr;
+    if (ld != in_dim || reinterpret_cast<uintptr_t>(q) % 16) {
+        BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&wpad), out_dim * ld, stream));
+        BD_CUDA(cudaMemsetAsync(wpad, 0, out_dim * ld, stream));
+        BD_CUDA(cudaMemcpy2DAsync(wpad, ld, q, in_dim, in_dim, out_dim, cudaMemcpyDeviceToDevice, stream));
+        wq = wpad;
+    }
+    const CUtensorMap mw = tmap_weights_i8(wq, out_dim, in_dim, ld);
+    constexpr int kChunk = 64;  // requests per launch (kPieces x 64 = 256 MMA columns)
+    const int bmax = int(std::min<uint64_t>(s, kChunk));
+    int8_t* xq = nullptr;
+    float* ps = nullptr;
+    BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&xq), size_t(kPieces) * bmax * ld, stream));
+    BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ps), sizeof(float) * kPieces * bmax, stream));
+    for (uint64_t b0 = 0; b0 < s; b0 += kChunk) {
+        const int nb = int(std::min<uint64_t>(kChunk, s - b0));
+        const GemmPlan g = plan_i8_gemm(out_dim, in_dim, nb);
+        float* P = nullptr;
+        BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&P), sizeof(float) * g.splits * nb * out_dim, stream));
+        quant_pieces_launch(A + b0 * in_dim, true, int(in_dim), int(in_dim), nb, xq, int(ld), ps, stream);
+        const CUtensorMap mx = tmap_pieces(xq, nb, in_dim, ld, g.bn);
+        i8_gemm_launch(g, mw, mx, row_scales, ps, P, stream);
+        combine_launch(P, g.splits, nullptr, nb, int(out_dim), Y + b0 * out_dim, stream);
+        BD_CUDA(cudaFreeAsync(P, stream));
+    }
+    BD_CUDA(cudaFreeAsync(xq, stream));
+    BD_CUDA(cudaFreeAsync(ps, stream));
+    if (wpad) BD_CUDA(cudaFreeAsync(wpad, stream));
+}
+
 }  // namespace bd
 
 using namespace bd;
@@ -380,6 +423,17 @@ int bd_delta_linear_backward(int32_t n_planes, const uint8_t* const* plane_bits,
             dot_f64_launch(dy, plane_u[pl], s * rows, scale_grad + pl, st);
             packed_transpose_launch(plane_bits[pl], rows, cols, dy, s, dx, scales[pl], false, st);
         }
+    });
+}
+
+int bd_rtn_quantize(const float* W, uint64_t rows, uint64_t cols, int8_t* q, float* row_scales, void* stream) {
+    return guarded([&] { rtn_quantize_launch(W, rows, cols, q, cols, row_scales, static_cast<cudaStream_t>(stream)); });
+}
+
+int bd_int8_matmul_nt(const float* A, uint64_t s, uint64_t in_dim, const int8_t* q, const float* row_scales,
+                      uint64_t out_dim, float* Y, void* stream) {
+    return guarded([&] {
+        int8_matmul_impl(A, s, in_dim, q, row_scales, out_dim, Y, static_cast<cudaStream_t>(stream));
     });
 }
 

@@ -47,10 +47,16 @@ __host__ __device__ inline GemmSmemLayout gemm_layout(int bn, int stages) {
     return L;
 }
 
+// kI8 (the INT8 RTN backbone of P:src/int8.cpp:67-81): W is the int8
+// RTN tensor, X holds kPieces int8 pieces per request (quant_pieces_kernel), the MMA is
+// kind::i8 (s8 x s8 -> exact s32) with K = 128 per 128-byte stage row, and the epilogue
+// recombines y = row_scale[m] * float(sum_p acc_p * piece_scale_p).
+template <bool kI8>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     base_gemm_kernel(const __grid_constant__ CUtensorMap map_w,
                      const __grid_constant__ CUtensorMap map_x, float* __restrict__ partial,
-                     int M, int N_valid, int bn, int kb_total, int kb_per_split, int stages) {
+                     int M, int N_valid, int bn, int kb_total, int kb_per_split, int stages,
+                     const float* __restrict__ row_scale, const float* __restrict__ piece_scale) {
     extern __shared__ uint8_t smem_raw[];
     const unsigned long long t_entry = gtimer();
     unsigned long long t_wait = 0;
@@ -100,7 +106,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int npre = min(nkb, stages);
         for (int i = 0; i < npre; ++i) {
             mbar_arrive_expect_tx(&full[i], L.stage_bytes);
-            tma_load_2d_hint(smem + i * L.stage_bytes, &map_w, &full[i], (kb0 + i) * kBK, m0, pol_w);
+            tma_load_2d_hint(smem + i * L.stage_bytes, &map_w, &full[i], (kb0 + i) * (kI8 ? 128 : kBK), m0, pol_w);
         }
         griddep_wait();  // PDL: the activations come from the previous kernel
         t_wait = gtimer();
@@ -109,7 +115,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const uint32_t round = i / stages;
             uint8_t* a = smem + s * L.stage_bytes;
             uint8_t* b = a + L.a_bytes;
-            const int kc = (kb0 + i) * kBK;
+            const int kc = (kb0 + i) * (kI8 ? 128 : kBK);
             if (i >= npre) {
                 mbar_wait(&empty[s], (round & 1) ^ 1);
                 mbar_arrive_expect_tx(&full[s], L.stage_bytes);
@@ -119,7 +125,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
     } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer ---- (consumes only what the producer's barriers release)
-        const uint32_t idesc = idesc_bf16_f32(kBM, bn);
+        const uint32_t idesc = kI8 ? idesc_s8s8_s32(kBM, bn) : idesc_bf16_f32(kBM, bn);
         for (int i = 0; i < nkb; ++i) {
             const int s = i % stages;
             const uint32_t round = i / stages;
@@ -129,8 +135,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             uint8_t* b = a + L.a_bytes;
             const uint64_t da = sdesc_k128(a), db = sdesc_k128(b);
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)  // +32 bytes per 16-wide K step
-                mma_bf16_ss(taddr, da + 2 * k, db + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < 4; ++k) {  // +32 bytes per K step (16 bf16 / 32 int8)
+                if (kI8) mma_i8_ss(taddr, da + 2 * k, db + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
+                else mma_bf16_ss(taddr, da + 2 * k, db + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
+            }
             tc_commit(&empty[s]);
         }
         tc_commit(done);
@@ -151,10 +159,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (int j = 0; j < 16; ++j) r[j] = 0;
         }
         if (row < M) {
+            if (kI8) {
+                // 16 columns = 4 requests x kPieces (4) int32 accumulators
+                const float rs = row_scale[row];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int n = c0 + j;
-                if (n < N_valid) out[static_cast<size_t>(n) * M + row] = __uint_as_float(r[j]);
+                for (int q = 0; q < 4; ++q) {
+                    const int n = c0 / kPieces + q;
+                    if (n >= N_valid) break;
+                    double acc = 0.0;  // exact: |acc_p| < 2^31, piece scales are powers of two
+#pragma unroll
+                    for (int pc = 0; pc < kPieces; ++pc)
+                        acc += static_cast<double>(static_cast<int32_t>(r[q * kPieces + pc])) *
+                               static_cast<double>(piece_scale[n * kPieces + pc]);
+                    out[static_cast<size_t>(n) * M + row] = static_cast<float>(acc) * rs;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int n = c0 + j;
+                    if (n < N_valid) out[static_cast<size_t>(n) * M + row] = __uint_as_float(r[j]);
+                }
             }
         }
     }
@@ -212,12 +236,22 @@ CUtensorMap make_tmap_2d(const void* ptr, CUtensorMapDataType dt, uint32_t elem_
 }
 
 GemmPlan plan_base_gemm(uint64_t M, uint64_t K, int batch, int smem_cap) {
+    return plan_gemm(M, K, batch, smem_cap, false);
+}
+GemmPlan plan_i8_gemm(uint64_t M, uint64_t K, int batch, int smem_cap) {
+    return plan_gemm(M, K, batch, smem_cap, true);
+}
+
+GemmPlan plan_gemm(uint64_t M, uint64_t K, int batch, int smem_cap, bool i8) {
     GemmPlan p;
     p.M = M;
     p.K = K;
     p.batch = batch;
-    p.bn = std::max(16, ((batch + 15) / 16) * 16);
-    require(p.bn <= 256, BD_ERR_BAD_ARGUMENT, "base gemm: batch chunk must be <= 256");
+    p.i8 = i8;
+    const int n_cols = i8 ? kPieces * batch : batch;  // int8: kPieces MMA columns per request
+    p.bn = std::max(16, ((n_cols + 15) / 16) * 16);
+    require(p.bn <= 256, BD_ERR_BAD_ARGUMENT,
+            i8 ? "int8 gemm: batch chunk must be <= 64" : "base gemm: batch chunk must be <= 256");
     const GemmSmemLayout L0 = gemm_layout(p.bn, 1);
     int slots;
     if (smem_cap > 0) {
@@ -235,7 +269,8 @@ GemmPlan plan_base_gemm(uint64_t M, uint64_t K, int batch, int smem_cap) {
     }
     p.smem = gemm_layout(p.bn, p.stages).total;
     const int m_tiles = int((M + kBM - 1) / kBM);
-    const int kb = int((K + kBK - 1) / kBK);
+    const int kbk = i8 ? 128 : kBK;  // K elements per 128-byte stage row
+    const int kb = int((K + kbk - 1) / kbk);
     // split-K to fill the machine: minimise ceil(tiles*s/slots) * ceil(kb/s)
     int best_s = 1;
     double best_cost = 1e30;
@@ -256,27 +291,48 @@ GemmPlan plan_base_gemm(uint64_t M, uint64_t K, int batch, int smem_cap) {
     return p;
 }
 
-void base_gemm_launch(const GemmPlan& p, const CUtensorMap& map_w, const CUtensorMap& map_x,
-                      float* partial, cudaStream_t stream) {
+template <bool kI8>
+static void gemm_launch_t(const GemmPlan& p, const CUtensorMap& map_w, const CUtensorMap& map_x,
+                          float* partial, const float* row_scale, const float* piece_scale, cudaStream_t stream) {
     static bool attr_set = false;
     if (!attr_set) {
-        BD_CUDA(cudaFuncSetAttribute(base_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        BD_CUDA(cudaFuncSetAttribute(base_gemm_kernel<kI8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      227 * 1024));
         // full carveout: an SM first configured for the co-resident K3 LUT must still
         // have room for a GEMM CTA (the default picks the smallest fitting carveout)
-        BD_CUDA(cudaFuncSetAttribute(base_gemm_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+        BD_CUDA(cudaFuncSetAttribute(base_gemm_kernel<kI8>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      int(cudaSharedmemCarveoutMaxShared)));
         attr_set = true;
     }
     dim3 grid(p.m_tiles, p.splits);
-    BD_CUDA(launch_pdl(base_gemm_kernel, grid, dim3(kGemmThreads), size_t(p.smem), stream, map_w, map_x, partial,
-                       int(p.M), p.batch, p.bn, p.kb_total, p.kb_per_split, p.stages));
+    BD_CUDA(launch_pdl(base_gemm_kernel<kI8>, grid, dim3(kGemmThreads), size_t(p.smem), stream, map_w, map_x,
+                       partial, int(p.M), p.batch, p.bn, p.kb_total, p.kb_per_split, p.stages, row_scale,
+                       piece_scale));
     note_launch();
     BD_CUDA(cudaGetLastError());
 }
 
+void base_gemm_launch(const GemmPlan& p, const CUtensorMap& map_w, const CUtensorMap& map_x,
+                      float* partial, cudaStream_t stream) {
+    require(!p.i8, BD_ERR_BAD_ARGUMENT, "base gemm: int8 plan on the bf16 kernel");
+    gemm_launch_t<false>(p, map_w, map_x, partial, nullptr, nullptr, stream);
+}
+
+void i8_gemm_launch(const GemmPlan& p, const CUtensorMap& map_wq, const CUtensorMap& map_xq,
+                    const float* row_scale, const float* piece_scale, float* partial, cudaStream_t stream) {
+    require(p.i8, BD_ERR_BAD_ARGUMENT, "int8 gemm: bf16 plan");
+    gemm_launch_t<true>(p, map_wq, map_xq, partial, row_scale, piece_scale, stream);
+}
+
 CUtensorMap tmap_weights(const void* W, uint64_t M, uint64_t K, uint64_t ld) {
     return make_tmap_2d(W, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, K, ld, kBM, kBK, true);
+}
+CUtensorMap tmap_weights_i8(const void* Wq, uint64_t M, uint64_t K, uint64_t ld) {
+    return make_tmap_2d(Wq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, M, K, ld, kBM, 128, true);
+}
+CUtensorMap tmap_pieces(const void* Xq, int batch, uint64_t K, uint64_t ld, int bn) {
+    return make_tmap_2d(Xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, uint64_t(kPieces) * batch, K, ld,
+                        uint32_t(bn), 128, true);
 }
 CUtensorMap tmap_acts(const void* X, int batch, uint64_t K, uint64_t ld, int bn) {
     return make_tmap_2d(X, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, uint64_t(batch), K, ld,

@@ -17,9 +17,15 @@ struct GemmPlan {
     uint64_t M = 0, K = 0;
     int batch = 0, bn = 16, stages = 4, smem = 0;
     int m_tiles = 0, kb_total = 0, kb_per_split = 0, splits = 1;
+    bool i8 = false;  // INT8 RTN backbone (kind::i8 against kPieces int8 pieces of X)
 };
+// int8 pieces per activation row (quant_pieces_launch): x = sum_p piece_scale_p * q_p with
+// |q_p| <= 64 and 7 bits per piece, i.e. x to 2^-27 of its row maximum (f32 has 24 bits)
+constexpr int kPieces = 4;
 // smem_cap > 0: plan one CTA per SM within smem_cap bytes (co-resident with the K3 LUT)
 GemmPlan plan_base_gemm(uint64_t M, uint64_t K, int batch, int smem_cap = 0);
+GemmPlan plan_i8_gemm(uint64_t M, uint64_t K, int batch, int smem_cap = 0);
+GemmPlan plan_gemm(uint64_t M, uint64_t K, int batch, int smem_cap, bool i8);
 CUtensorMap make_tmap_2d(const void* ptr, CUtensorMapDataType dt, uint32_t elem_bytes,
                          uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
                          uint32_t box_rows, uint32_t box_cols, bool swizzle128);
@@ -28,6 +34,20 @@ CUtensorMap tmap_acts(const void* X, int batch, uint64_t K, uint64_t ld, int bn)
 // partial: [splits][batch][M] f32
 void base_gemm_launch(const GemmPlan& p, const CUtensorMap& map_w, const CUtensorMap& map_x,
                       float* partial, cudaStream_t stream);
+// ---- K2 int8 (int8_matmul_nt, P:src/int8.cpp:67-81) ----
+// Wq: int8 [M x K] (row stride ld bytes, % 16 == 0); Xq: kPieces rows per request
+CUtensorMap tmap_weights_i8(const void* Wq, uint64_t M, uint64_t K, uint64_t ld);
+CUtensorMap tmap_pieces(const void* Xq, int batch, uint64_t K, uint64_t ld, int bn);
+// partial[s][b][m] = row_scale[m] * float(sum_p piece_scale[b*kPieces+p] * (Wq[m] . Xq[b*kPieces+p]))
+void i8_gemm_launch(const GemmPlan& p, const CUtensorMap& map_wq, const CUtensorMap& map_xq,
+                    const float* row_scale, const float* piece_scale, float* partial, cudaStream_t stream);
+// X (bf16 or f32 [batch x ldx], K valid columns) -> Xq int8 [batch*kPieces x ldq] (columns
+// >= K zeroed up to ldq) and piece_scale [batch*kPieces] (powers of two)
+void quant_pieces_launch(const void* X, bool x_f32, int ldx, int K, int batch, int8_t* Xq, int ldq,
+                         float* piece_scale, cudaStream_t stream);
+// RTN quantize (P:src/int8.cpp:15-42): per row s = amax/127, q = clamp(nearbyint(double(w)/s))
+void rtn_quantize_launch(const float* W, uint64_t rows, uint64_t cols, int8_t* q, uint64_t ldq,
+                         float* row_scales, cudaStream_t stream);
 
 // ---- K1 compressor ----
 void compress_launch(const bd_compress_job* jobs, int n_jobs, bd_dtype dtype, cudaStream_t s);
