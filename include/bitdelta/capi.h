@@ -199,6 +199,15 @@ int bd_pool_init_loopback(bd_pool* pool, const char* group);
 int bd_pool_set_tensor(bd_pool* pool, const char* name, const void* data, bd_dtype dtype,
                        int is_device, uint64_t rows, uint64_t cols);
 
+/* INT8 RTN backbone (ServingPool(QuantizedCheckpoint), P:src/serve.cpp:99-108, 120-125):
+ * one of the 7 layer projections as an Int8Tensor (P:include/deltakit/int8.hpp: int8 values
+ * [rows x cols] + f32 row scales, e.g. from bd_rtn_quantize), full (unsharded) shape; host
+ * memory unless is_device != 0. A pool's projections are all int8 or all dense (the other
+ * tensors stay dense); its K2 runs tcgen05 kind::i8 (half the backbone bytes of bf16) and
+ * serves batches of <= 64. */
+int bd_pool_set_tensor_i8(bd_pool* pool, const char* name, const int8_t* q, const float* row_scales,
+                          int is_device, uint64_t rows, uint64_t cols);
+
 /* One tensor of a tenant's delta (DeltaEntry, delta.hpp:76-86). */
 typedef struct bd_delta_entry {
     const char* name;

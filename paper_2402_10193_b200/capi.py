@@ -61,7 +61,7 @@ class PoolStats(C.Structure):
 SYMBOLS = [
     "bd_abi_version", "bd_last_error", "bd_device_check", "bd_launch_count", "bd_packed_size",
     "bd_compress", "bd_compress_batched", "bd_compress_stack", "bd_packed_signed_accumulate",
-    "bd_packed_matvec", "bd_packed_signed_accumulate_t", "bd_delta_linear_backward", "bd_rtn_quantize", "bd_int8_matmul_nt", "bd_multitenant_linear", "bd_multitenant_linear_f32", "bd_pool_create", "bd_pool_destroy",
+    "bd_packed_matvec", "bd_packed_signed_accumulate_t", "bd_delta_linear_backward", "bd_rtn_quantize", "bd_int8_matmul_nt", "bd_pool_set_tensor_i8", "bd_multitenant_linear", "bd_multitenant_linear_f32", "bd_pool_create", "bd_pool_destroy",
     "bd_pool_set_tensor", "bd_pool_register_delta", "bd_pool_register_delta_file",
     "bd_bdelta_validate", "bd_pool_open_request", "bd_pool_close_request", "bd_pool_decode_step",
     "bd_pool_decode_layers", "bd_pool_get_stats", "bd_pool_profile_layers", "bd_pool_profile_layers_serial", "bd_nccl_unique_id",
@@ -97,6 +97,7 @@ def lib() -> C.CDLL:
     L.bd_pool_destroy.argtypes = [vp]
     L.bd_pool_destroy.restype = None
     L.bd_pool_set_tensor.argtypes = [vp, C.c_char_p, vp, C.c_int, C.c_int, u64, u64]
+    L.bd_pool_set_tensor_i8.argtypes = [vp, C.c_char_p, vp, vp, C.c_int, u64, u64]
     L.bd_pool_register_delta.argtypes = [vp, C.c_char_p, C.POINTER(DeltaEntry), C.c_int]
     L.bd_pool_register_delta_file.argtypes = [vp, C.c_char_p, C.c_char_p, C.c_int]
     L.bd_pool_open_request.argtypes = [vp, C.c_char_p, C.POINTER(u64)]

@@ -67,6 +67,8 @@ bd_pool* pool_create(const bd_arch& a, int device, int world, int rank);
 void pool_destroy(bd_pool* p);
 void pool_set_tensor(bd_pool* p, const char* name, const void* data, bd_dtype dt, int is_dev,
                      uint64_t rows, uint64_t cols);
+void pool_set_tensor_i8(bd_pool* p, const char* name, const int8_t* q, const float* scales, int is_dev,
+                        uint64_t rows, uint64_t cols);
 void pool_register(bd_pool* p, const char* id, const bd_delta_entry* e, int n);
 void pool_register_file(bd_pool* p, const char* id, const char* path, int resident);
 uint64_t pool_open(bd_pool* p, const char* id);
@@ -519,6 +521,13 @@ int bd_pool_set_tensor(bd_pool* pool, const char* name, const void* data, bd_dty
     return guarded([&] {
         require(pool != nullptr, BD_ERR_BAD_ARGUMENT, "null pool");
         pool_set_tensor(pool, name, data, dtype, is_device, rows, cols);
+    });
+}
+int bd_pool_set_tensor_i8(bd_pool* pool, const char* name, const int8_t* q, const float* row_scales,
+                          int is_device, uint64_t rows, uint64_t cols) {
+    return guarded([&] {
+        require(pool != nullptr, BD_ERR_BAD_ARGUMENT, "null pool");
+        pool_set_tensor_i8(pool, name, q, row_scales, is_device, rows, cols);
     });
 }
 int bd_pool_register_delta(bd_pool* pool, const char* id, const bd_delta_entry* entries,

@@ -127,8 +127,13 @@ struct Request {
 };
 
 struct LayerW {
-    uint16_t *qkv = nullptr, *o = nullptr, *gu = nullptr, *down = nullptr;
+    uint16_t *qkv = nullptr, *o = nullptr, *gu = nullptr, *down = nullptr;  // bf16 backbone
     CUtensorMap m_qkv, m_o, m_gu, m_down;
+    // INT8 RTN backbone (ServingPool(QuantizedCheckpoint), P:src/serve.cpp:99-108): per
+    // projection group (qkv, o, gu, down) stacked int8 rows + f32 row scales
+    int8_t* q8[4] = {nullptr, nullptr, nullptr, nullptr};
+    float* s8[4] = {nullptr, nullptr, nullptr, nullptr};
+    CUtensorMap m8[4];
 };
 
 struct Plan {
@@ -150,6 +155,7 @@ struct Plan {
     std::vector<DeltaUnit> lm_units;
     GemmPlan g_qkv, g_o, g_gu, g_down, g_lm;
     CUtensorMap x_xn, x_ctx, x_act;  // B-operand maps for this batch size
+    CUtensorMap xq_dim, xq_inter;    // int8 backbone: activation pieces (quant_pieces_launch)
     // byte-LUT deltas (few requests per tenant) per layer & group; one launch per
     // kLutMaxJobs requests (each launch writes its own requests' rows of D)
     struct Lut {
@@ -178,6 +184,10 @@ struct PoolImpl {
     uint64_t q_r0 = 0, kv_r0 = 0, dim_r0 = 0, inter_r0 = 0;
     uint64_t ld_dim = 0, ld_inter = 0;  // padded strides (elements)
     std::vector<LayerW> L;
+    int base_kind = 0;                  // projections: 0 = none set yet, 1 = bf16, 2 = int8 RTN
+    uint64_t ld8_dim = 0, ld8_inter = 0;  // int8 row strides (TMA: multiples of 16 bytes)
+    int8_t* xq = nullptr;                 // int8 activation pieces [kPieces * ws_B][ld8 max]
+    float* xps = nullptr;                 // their scales [kPieces * ws_B]
     std::vector<std::vector<float>> base_norm1, base_norm2;  // host copies (full)
     std::vector<float> base_final_norm;
     float* embed = nullptr;
@@ -288,21 +298,10 @@ struct PoolImpl {
         BD_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
         if (const char* e = std::getenv("BD_DELTA")) delta_mode = e;
 
+        ld8_dim = round_up(a.dim, 16);
+        ld8_inter = round_up(a.intermediate, 16);
+        // layer buffers are allocated with the first projection tensor: bf16 or int8
         L.resize(a.n_layers);
-        for (auto& l : L) {
-            l.qkv = dmalloc<uint16_t>((q_l + 2 * kv_l) * ld_dim, &allocs);
-            l.o = dmalloc<uint16_t>(dim_l * ld_dim, &allocs);
-            l.gu = dmalloc<uint16_t>(2 * inter_l * ld_dim, &allocs);
-            l.down = dmalloc<uint16_t>(dim_l * ld_inter, &allocs);
-            BD_CUDA(cudaMemset(l.qkv, 0, (q_l + 2 * kv_l) * ld_dim * 2));
-            BD_CUDA(cudaMemset(l.o, 0, dim_l * ld_dim * 2));
-            BD_CUDA(cudaMemset(l.gu, 0, 2 * inter_l * ld_dim * 2));
-            BD_CUDA(cudaMemset(l.down, 0, dim_l * ld_inter * 2));
-            l.m_qkv = tmap_weights(l.qkv, q_l + 2 * kv_l, a.dim, ld_dim);
-            l.m_o = tmap_weights(l.o, dim_l, a.dim, ld_dim);
-            l.m_gu = tmap_weights(l.gu, 2 * inter_l, a.dim, ld_dim);
-            l.m_down = tmap_weights(l.down, dim_l, a.intermediate, ld_inter);
-        }
         embed = dmalloc<float>(a.vocab * a.dim, &allocs);
         lm_head = dmalloc<uint16_t>(a.vocab * ld_dim, &allocs);
         BD_CUDA(cudaMemset(lm_head, 0, a.vocab * ld_dim * 2));
@@ -379,6 +378,76 @@ struct PoolImpl {
         }
     }
 
+    void ensure_dense(LayerW& l) {
+        if (l.qkv) return;
+        l.qkv = dmalloc<uint16_t>((q_l + 2 * kv_l) * ld_dim, &allocs);
+        l.o = dmalloc<uint16_t>(dim_l * ld_dim, &allocs);
+        l.gu = dmalloc<uint16_t>(2 * inter_l * ld_dim, &allocs);
+        l.down = dmalloc<uint16_t>(dim_l * ld_inter, &allocs);
+        BD_CUDA(cudaMemset(l.qkv, 0, (q_l + 2 * kv_l) * ld_dim * 2));
+        BD_CUDA(cudaMemset(l.o, 0, dim_l * ld_dim * 2));
+        BD_CUDA(cudaMemset(l.gu, 0, 2 * inter_l * ld_dim * 2));
+        BD_CUDA(cudaMemset(l.down, 0, dim_l * ld_inter * 2));
+        l.m_qkv = tmap_weights(l.qkv, q_l + 2 * kv_l, a.dim, ld_dim);
+        l.m_o = tmap_weights(l.o, dim_l, a.dim, ld_dim);
+        l.m_gu = tmap_weights(l.gu, 2 * inter_l, a.dim, ld_dim);
+        l.m_down = tmap_weights(l.down, dim_l, a.intermediate, ld_inter);
+    }
+    // rows of group g (qkv, o, gu, down) and its K
+    uint64_t group_rows(int g) const {
+        return g == 0 ? q_l + 2 * kv_l : g == 2 ? 2 * inter_l : dim_l;
+    }
+    uint64_t group_k(int g) const { return g == 3 ? a.intermediate : a.dim; }
+    void ensure_i8(LayerW& l) {
+        if (l.q8[0]) return;
+        for (int g = 0; g < 4; ++g) {
+            const uint64_t rows = group_rows(g), ld8 = g == 3 ? ld8_inter : ld8_dim;
+            l.q8[g] = dmalloc<int8_t>(rows * ld8, &allocs);
+            l.s8[g] = dmalloc<float>(rows, &allocs);
+            BD_CUDA(cudaMemset(l.q8[g], 0, rows * ld8));
+            BD_CUDA(cudaMemset(l.s8[g], 0, rows * 4));
+            l.m8[g] = tmap_weights_i8(l.q8[g], rows, group_k(g), ld8);
+        }
+    }
+    static int proj_group(int role) {
+        return role <= P_V ? 0 : role == P_O ? 1 : role <= P_UP ? 2 : 3;
+    }
+    void set_base_kind(int kind, const std::string& name) {
+        require(base_kind == 0 || base_kind == kind, BD_ERR_UNSUPPORTED_DTYPE,
+                "tensor '" + name + "': a pool's projections are all int8 or all dense");
+        base_kind = kind;
+    }
+
+    // INT8 RTN projection (Int8Tensor, P:include/deltakit/int8.hpp: values + row scales),
+    // the backbone of ServingPool(QuantizedCheckpoint) (serve.cpp:99-108, 120-125)
+    void set_tensor_i8(const std::string& name, const int8_t* q, const float* scales, bool is_dev,
+                       uint64_t rows, uint64_t cols) {
+        const int idx = tindex(name);
+        require(idx >= 0, BD_ERR_NAME_MISMATCH, "backbone: unknown tensor '" + name + "'");
+        uint64_t er, ec;
+        shape(idx, er, ec);
+        require(rows == er && cols == ec, BD_ERR_SHAPE_MISMATCH,
+                "backbone: tensor '" + name + "' has shape " + std::to_string(rows) + "x" +
+                    std::to_string(cols) + ", config expects " + std::to_string(er) + "x" +
+                    std::to_string(ec));
+        const size_t last = 1 + 9 * a.n_layers;
+        const int role = (idx >= 1 && size_t(idx) < last) ? (idx - 1) % 9 : -1;
+        require(role >= 0 && role < 7, BD_ERR_UNSUPPORTED_DTYPE,
+                "tensor '" + name + "': only the 7 layer projections may be int8 on the device");
+        set_base_kind(2, name);
+        BD_CUDA(cudaSetDevice(device));
+        const int l = (idx - 1) / 9, g = proj_group(role);
+        ensure_i8(L[l]);
+        uint64_t r0, nr;
+        local_rows(role, r0, nr);
+        const uint64_t ld8 = g == 3 ? ld8_inter : ld8_dim;
+        const cudaMemcpyKind k = is_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        BD_CUDA(cudaMemcpy2D(L[l].q8[g] + stack_offset(role) * ld8, ld8, q + r0 * cols, cols, cols, nr, k));
+        BD_CUDA(cudaMemcpy(L[l].s8[g] + stack_offset(role), scales + r0, nr * 4, k));
+        if (!have[idx]) backbone_bytes = backbone_bytes - 4ull * rows * cols + rows * cols + 4ull * rows;
+        have[idx] = true;
+    }
+
     void upload_bf16(uint16_t* dst, uint64_t ldd, const void* src, bd_dtype dt, bool is_dev,
                      uint64_t rows, uint64_t cols, uint64_t src_row0) {
         const size_t es = dt == BD_BF16 ? 2 : 4;
@@ -444,6 +513,8 @@ struct PoolImpl {
             if (role == 7) base_norm1[l] = to_host_f32(data, dt, is_dev, cols);
             else if (role == 8) base_norm2[l] = to_host_f32(data, dt, is_dev, cols);
             else {
+                set_base_kind(1, name);
+                ensure_dense(L[l]);
                 uint64_t r0, nr;
                 local_rows(role, r0, nr);
                 uint16_t* buf;
@@ -706,6 +777,11 @@ struct PoolImpl {
         P = dmalloc<float>(P_elems, &ws_allocs);
         logits = dmalloc<float>(ws_B * a.vocab, &ws_allocs);
         msq = dmalloc<char>(norm_ws_bytes(int(ws_B), int(a.dim)), &ws_allocs);
+        if (base_kind == 2) {
+            xq = dmalloc<int8_t>(size_t(kPieces) * ws_B * std::max(ld8_dim, ld8_inter), &ws_allocs);
+            xps = dmalloc<float>(size_t(kPieces) * ws_B, &ws_allocs);
+            BD_CUDA(cudaMemset(xq, 0, size_t(kPieces) * ws_B * std::max(ld8_dim, ld8_inter)));
+        }
         BD_CUDA(cudaMemset(msq, 0, norm_ws_bytes(int(ws_B), int(a.dim))));
         if (world > 1) {
             ctx_loc = dmalloc<uint16_t>(size_t(ws_B) * q_l, &ws_allocs);
@@ -976,24 +1052,31 @@ struct PoolImpl {
                 p->lm_units.push_back(u);
             }
         }
-        p->g_qkv = plan_base_gemm(q_l + 2 * kv_l, a.dim, B);
-        p->g_o = plan_base_gemm(dim_l, a.dim, B);
-        p->g_gu = plan_base_gemm(2 * inter_l, a.dim, B);
-        p->g_down = plan_base_gemm(dim_l, a.intermediate, B);
+        const bool i8 = base_kind == 2;
+        require(!i8 || B <= 64, BD_ERR_BAD_ARGUMENT, "decode: an int8 backbone serves batches of <= 64");
+        p->g_qkv = plan_gemm(q_l + 2 * kv_l, a.dim, B, 0, i8);
+        p->g_o = plan_gemm(dim_l, a.dim, B, 0, i8);
+        p->g_gu = plan_gemm(2 * inter_l, a.dim, B, 0, i8);
+        p->g_down = plan_gemm(dim_l, a.intermediate, B, 0, i8);
         p->g_lm = plan_base_gemm(a.vocab, a.dim, B);
         for (const GemmPlan* g : {&p->g_qkv, &p->g_o, &p->g_gu, &p->g_down, &p->g_lm})
             require(uint64_t(g->splits) * B * g->M <= P_elems, BD_ERR_CUDA, "split-K workspace too small");
-        const int bn = p->g_qkv.bn;
+        const int bn = p->g_lm.bn;  // bf16 B operand (lm_head is always bf16)
         p->x_xn = tmap_acts(xn, B, a.dim, ld_dim, bn);
         p->x_ctx = tmap_acts(ctx, B, a.dim, ld_dim, bn);
         p->x_act = tmap_acts(act, B, a.intermediate, ld_inter, bn);
+        if (i8) {
+            p->xq_dim = tmap_pieces(xq, B, a.dim, ld8_dim, p->g_qkv.bn);
+            p->xq_inter = tmap_pieces(xq, B, a.intermediate, ld8_inter, p->g_qkv.bn);
+        }
         // K3 variant for the whole batch (one backend, chosen by requests per tenant): K23
         // when tenants average k23_min_requests(B) requests or more (each plane is then read
         // once per slot of up to 4 requests), the byte LUT beside K2 otherwise (one job per
         // request); the mean, not the maximum, so one busy tenant does not move a batch of
         // single-request tenants onto K23 (measured slower there)
         const double mean_per_tenant = order.empty() ? 0.0 : double(B) / double(order.size());
-        if (delta_mode == "mt4" || (delta_mode == "auto" && mean_per_tenant >= k23_min_requests(B)))
+        // K23 fuses the bf16 base GEMM: not for an int8 backbone
+        if (!i8 && (delta_mode == "mt4" || (delta_mode == "auto" && mean_per_tenant >= k23_min_requests(B))))
             plan_mt4_groups(*p, by_t);
         if (delta_mode == "lut" || delta_mode == "auto") plan_lut_groups(*p);
         // groups already served by K23 keep no LUT plan
@@ -1006,7 +1089,7 @@ struct PoolImpl {
             GemmPlan* gs[4] = {&p->g_qkv, &p->g_o, &p->g_gu, &p->g_down};
             for (int gi = 0; gi < 4; ++gi)
                 if (p->lut[0][gi].ok) {
-                    *gs[gi] = plan_base_gemm(gs[gi]->M, gs[gi]->K, B, 88 * 1024);
+                    *gs[gi] = plan_gemm(gs[gi]->M, gs[gi]->K, B, 88 * 1024, i8);
                     require(uint64_t(gs[gi]->splits) * B * gs[gi]->M <= P_elems, BD_ERR_CUDA,
                             "split-K workspace too small");
                 }
@@ -1068,9 +1151,24 @@ struct PoolImpl {
         return proj_out(g, true);
     }
 
+    // K2 for one projection group: the bf16 tcgen05 GEMM, or (int8 backbone) the kind::i8
+    // GEMM against the pieces quant_pieces_launch wrote for this linear's input
+    void base_gemm(const GemmPlan& g, uint64_t l, int group, const CUtensorMap& mw, const CUtensorMap& mx,
+                   cudaStream_t st) {
+        if (g.i8) i8_gemm_launch(g, mw, mx, L[l].s8[group], xps, P, st);
+        else base_gemm_launch(g, mw, mx, P, st);
+    }
+
     void linear(Plan& p, uint64_t l, int group, const GemmPlan& g, const CUtensorMap& mw,
                 const CUtensorMap& mx, const std::vector<DeltaUnit>& units, const uint16_t* X,
                 int ldx, int cols, int B, cudaStream_t s) {
+        if (g.i8) {
+            // the pieces buffer is free: the previous linear's K2 joined stream s before its
+            // consumer ran
+            prof(BD_PROF_XQ_PREP, s, [&] {
+                quant_pieces_launch(X, false, ldx, cols, B, xq, int(group == 3 ? ld8_inter : ld8_dim), xps, s);
+            });
+        }
         if (mt4_ok(p, l, group)) {
             prof(BD_PROF_XQ_PREP, s, [&] { xp_prep_launch(X, ldx, cols, B, p.xpk, s); });
             prof(BD_PROF_FUSED_QKV + group, s, [&] { mt4_launch(p.mt4[l][group].prm, s); });
@@ -1086,20 +1184,20 @@ struct PoolImpl {
                     BD_CUDA(cudaEventRecord(ev_fork, s));
                     BD_CUDA(cudaStreamWaitEvent(stream2, ev_fork, 0));
                     for (const LutParams& lp : luts) lut_launch(lp, X, D, s);
-                    base_gemm_launch(g, mw, mx, P, stream2);
+                    base_gemm(g, l, group, mw, mx, stream2);
                     BD_CUDA(cudaEventRecord(ev_join, stream2));
                     BD_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
                 });
                 return;
             }
             // serial (profile_layers_serial): K2 and K3 timed on their own
-            prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm_launch(g, mw, mx, P, s); });
+            prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm(g, l, group, mw, mx, s); });
             prof(BD_PROF_DELTA_QKV + group, s, [&] {
                 for (const LutParams& lp : luts) lut_launch(lp, X, D, s);
             });
             return;
         }
-        prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm_launch(g, mw, mx, P, s); });
+        prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm(g, l, group, mw, mx, s); });
         prof(BD_PROF_DELTA_QKV + group, s, [&] {
             delta_units_launch(units.data(), int(units.size()), X, ldx, cols, B, D, int(g.M), s);
         });
@@ -1162,28 +1260,32 @@ struct PoolImpl {
                 resid_norm_launch(x, B, int(a.dim), prev, p.d_norm + (2 * l) * B, xn, int(ld_dim),
                                   nullptr, msq, s);
             });
-            linear(p, l, 0, p.g_qkv, W.m_qkv, p.x_xn, p.units[l][0], xn, int(ld_dim), int(a.dim), B, s);
+            const bool i8 = base_kind == 2;
+            linear(p, l, 0, p.g_qkv, i8 ? W.m8[0] : W.m_qkv, i8 ? p.xq_dim : p.x_xn, p.units[l][0], xn,
+                   int(ld_dim), int(a.dim), B, s);
             aa.layer = int(l);
             prof(BD_PROF_ATTN, s, [&] {
                 attn_launch(group_out(p, l, 0, p.g_qkv), aa, p.d_pos, B, tp ? ctx_loc : ctx,
                             tp ? int(q_l) : int(ld_dim), s);
             });
             if (tp) exchange_bf16(ctx_loc, B, int(q_l), ctx, int(ld_dim), s);
-            linear(p, l, 1, p.g_o, W.m_o, p.x_ctx, p.units[l][1], ctx, int(ld_dim), int(a.dim), B, s);
+            linear(p, l, 1, p.g_o, i8 ? W.m8[1] : W.m_o, i8 ? p.xq_dim : p.x_ctx, p.units[l][1], ctx,
+                   int(ld_dim), int(a.dim), B, s);
             const ProjOut o_out = tp ? exchange_f32(group_out(p, l, 1, p.g_o), B, int(dim_l), s)
                                      : group_out(p, l, 1, p.g_o);
             prof(BD_PROF_NORM, s, [&] {
                 resid_norm_launch(x, B, int(a.dim), o_out, p.d_norm + (2 * l + 1) * B, xn, int(ld_dim),
                                   nullptr, msq, s);
             });
-            linear(p, l, 2, p.g_gu, W.m_gu, p.x_xn, p.units[l][2], xn, int(ld_dim), int(a.dim), B, s);
+            linear(p, l, 2, p.g_gu, i8 ? W.m8[2] : W.m_gu, i8 ? p.xq_dim : p.x_xn, p.units[l][2], xn,
+                   int(ld_dim), int(a.dim), B, s);
             prof(BD_PROF_SILU, s, [&] {
                 silu_launch(group_out(p, l, 2, p.g_gu), B, int(inter_l), tp ? act_loc : act,
                             tp ? int(inter_l) : int(ld_inter), s);
             });
             if (tp) exchange_bf16(act_loc, B, int(inter_l), act, int(ld_inter), s);
-            linear(p, l, 3, p.g_down, W.m_down, p.x_act, p.units[l][3], act, int(ld_inter),
-                   int(a.intermediate), B, s);
+            linear(p, l, 3, p.g_down, i8 ? W.m8[3] : W.m_down, i8 ? p.xq_inter : p.x_act, p.units[l][3], act,
+                   int(ld_inter), int(a.intermediate), B, s);
             prev = tp ? exchange_f32(group_out(p, l, 3, p.g_down), B, int(dim_l), s)
                       : group_out(p, l, 3, p.g_down);
         }
@@ -1404,6 +1506,11 @@ void pool_set_tensor(bd_pool* p, const char* name, const void* data, bd_dtype dt
                      uint64_t rows, uint64_t cols) {
     require(name && data, BD_ERR_BAD_ARGUMENT, "set_tensor: null argument");
     p->impl.set_tensor(name, data, dt, is_dev != 0, rows, cols);
+}
+void pool_set_tensor_i8(bd_pool* p, const char* name, const int8_t* q, const float* scales, int is_dev,
+                        uint64_t rows, uint64_t cols) {
+    require(name && q && scales, BD_ERR_BAD_ARGUMENT, "set_tensor_i8: null argument");
+    p->impl.set_tensor_i8(name, q, scales, is_dev != 0, rows, cols);
 }
 void pool_register(bd_pool* p, const char* id, const bd_delta_entry* e, int n) {
     require(id && (e || n == 0), BD_ERR_BAD_ARGUMENT, "register_delta: null argument");

@@ -10,6 +10,8 @@ import numpy as np
 from .capi import BD_BF16, BD_F32, Arch, DeltaEntry, PoolStats, Request, check, lib
 
 SHARED, NAIVE = "shared", "naive"  # ServeMode (serve.hpp:18)
+# default_quantize_policy (P:src/delta.cpp:150-161): the 7 layer projections
+PROJECTIONS = ("attn_q", "attn_k", "attn_v", "attn_o", "mlp_gate", "mlp_up", "mlp_down")
 
 
 def tensor_shapes(arch: Mapping) -> list[tuple[str, int, int]]:
@@ -31,7 +33,11 @@ class ServingPool:
     backbone pass per step for the whole batch (serve.cpp:205-325)."""
 
     def __init__(self, arch: Mapping, tensors: Mapping | None = None, device: int = 0,
-                 world_size: int = 1, rank: int = 0):
+                 world_size: int = 1, rank: int = 0, int8: bool = False):
+        """int8=True: ServingPool(QuantizedCheckpoint) (serve.cpp:99-108) built like
+        rtn_quantize_checkpoint(base, default_quantize_policy()) — the 7 layer projections
+        RTN-quantized on the device (bd_rtn_quantize), everything else dense. A tensor given
+        as a (int8 values, f32 row scales) pair is taken as already quantized."""
         self.arch = dict(arch)
         self.arch.setdefault("kv_dim", self.arch["dim"])
         self.arch.setdefault("rope_theta", 10000.0)
@@ -46,7 +52,34 @@ class ServingPool:
         self._ids: list[str] = []
         if tensors is not None:
             for name, t in tensors.items():
-                self.set_tensor(name, t)
+                if isinstance(t, tuple):
+                    self.set_tensor_i8(name, *t)
+                elif int8 and name.split(".")[-1] in PROJECTIONS:
+                    self.set_tensor_i8(name, *self._rtn(t))
+                else:
+                    self.set_tensor(name, t)
+
+    def _rtn(self, data):
+        import torch
+
+        from . import rtn_quantize
+
+        t = data if isinstance(data, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(data, np.float32))
+        return rtn_quantize(t.float().to(f"cuda:{self.device}"))
+
+    def set_tensor_i8(self, name: str, q, row_scales) -> None:
+        """One projection as an Int8Tensor (int8.hpp): int8 [rows, cols] + f32 [rows]."""
+        import torch
+
+        if isinstance(q, torch.Tensor):
+            qq, ss = q.contiguous(), row_scales.float().contiguous()
+            check(lib().bd_pool_set_tensor_i8(self._h, name.encode(), qq.data_ptr(), ss.data_ptr(), int(qq.is_cuda),
+                                              qq.shape[0], qq.shape[1]))
+        else:
+            qq = np.ascontiguousarray(q, np.int8)
+            ss = np.ascontiguousarray(row_scales, np.float32)
+            check(lib().bd_pool_set_tensor_i8(self._h, name.encode(), qq.ctypes.data, ss.ctypes.data, 0,
+                                              qq.shape[0], qq.shape[1]))
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -81,10 +81,24 @@ def port_logits(port, arch, flat, tenants, req_tenant, tokens, pos, kc, vc, thre
         return np.stack(list(ex.map(one, range(len(req_tenant)))))
 
 
-def run_config(port, arch, n_tenants, batch, steps=2, seed=0, planes=lambda t: 1, expect_paths=None):
+def run_config(port, arch, n_tenants, batch, steps=2, seed=0, planes=lambda t: 1, expect_paths=None,
+               int8=False):
+    """int8: the INT8 RTN backbone (ServingPool(QuantizedCheckpoint), serve.cpp:99-108): the 7
+    projections quantized by the reference rule (port.rtn_quantize, bit-exact with the
+    device's), the oracle run on rtn_dequantize (int8.cpp:44-53) of the same values."""
     arch = dict(arch, vocab=256, max_seq=8, rope_theta=10000.0)
     tens, tenants = synth_universe(arch, n_tenants, seed, planes)
+    if int8:
+        for name in list(tens):
+            if name.split(".")[-1] in PROJ:
+                q, sc = port.rtn_quantize(tens[name])
+                tens[name] = (q, sc)
     pool = ServingPool(arch, tens)
+    if int8:
+        for name in list(tens):
+            if isinstance(tens[name], tuple):
+                q, sc = tens[name]
+                tens[name] = q.astype(np.float32) * sc[:, None]
     for t, ents in enumerate(tenants):
         pool.register_delta_entries(f"t{t}", ents)
     req_tenant = [b % n_tenants for b in range(batch)]  # round robin (serve.cpp:410)
@@ -144,3 +158,15 @@ def test_multi_plane_stacks_default_paths(cuda, port, planes, tenants, batch):
     paths = "LLLL" if batch == tenants else "TTTT"
     assert run_config(port, arch, tenants, batch, steps=3, seed=5, planes=lambda t: planes[t % 2],
                       expect_paths=paths) <= 1e-2
+
+
+def test_int8_backbone_l7_layer_T8_B8(cuda, port):
+    """the configs[1] layer on an INT8 RTN backbone (K2 kind::i8 beside the
+    byte LUT) against the oracle on the dequantized backbone."""
+    assert run_config(port, dict(L7, n_layers=1), 8, 8, steps=3, expect_paths="LLLL", int8=True) <= 1e-2
+
+
+def test_int8_backbone_m7_gqa_B64_T16(cuda, port):
+    """int8 backbone at batch 64 (256 MMA columns of pieces), GQA, 4 requests per tenant: the
+    LUT (K23 fuses a bf16 GEMM and is not planned for an int8 backbone)."""
+    assert run_config(port, dict(M7, n_layers=1), 16, 64, steps=1, expect_paths="LLLL", int8=True) <= 1e-2

@@ -379,3 +379,47 @@ def test_multi_plane_reference_bdelta(cuda, B, paths):
         for i in range(B):
             assert rel_l2(got[i], want[i]) <= 1e-2, (pos, i, rel_l2(got[i], want[i]))
     pool.close()
+
+
+def test_int8_backbone_toy_matches_port(cuda, toy, port):
+    """ServingPool(QuantizedCheckpoint) (serve.cpp:99-108): the reference's own tenants on an
+    RTN-int8 backbone (rtn_quantize_checkpoint with default_quantize_policy: the 7 projections),
+    built on the device (ServingPool(..., int8=True) -> bd_rtn_quantize), against the port on
+    rtn_dequantize of the same values; backbone residency shrinks (int8 + row scales)."""
+    from paper_2402_10193_b200.serving import PROJECTIONS
+
+    d, arch = toy
+    base16 = bf16_round(d["base"])
+    tens = tensors_of(arch, base16)
+    names = [n for n, _, _ in tensor_shapes(arch)]
+    deq = dict(tens)
+    for n in names:
+        if n.split(".")[-1] in PROJECTIONS:
+            q, sc = port.rtn_quantize(tens[n])
+            deq[n] = q.astype(np.float32) * sc[:, None]
+    flat = np.concatenate([deq[n].reshape(-1) for n in names])
+    tenants = [[bdelta.read(os.path.join(GOLDEN, f"toy_t{i}.bdelta"))[n] for n in names] for i in range(4)]
+    dense = ServingPool(arch, tens)
+    pool = ServingPool(arch, tens, int8=True)
+    for i in range(4):
+        pool.register_delta(f"t{i}", os.path.join(GOLDEN, f"toy_t{i}.bdelta"))
+    B = 4
+    rids = [pool.open_request(f"t{i}") for i in range(B)]
+    kc = [np.zeros((arch["n_layers"], arch["max_seq"], arch["kv_dim"]), np.float32) for _ in range(B)]
+    vc = [np.zeros_like(k) for k in kc]
+    for pos, tok in enumerate(d["B4_tokens"]):
+        got = pool.decode_step([(r, int(tok), pos) for r in rids])
+        want = port.decode(arch, flat, tenants, list(range(B)), [int(tok)] * B, [pos] * B, kc, vc)
+        for i in range(B):
+            assert rel_l2(got[i], want[i]) <= 5e-3, (pos, i, rel_l2(got[i], want[i]))
+    for i in range(4):
+        dense.register_delta(f"t{i}", os.path.join(GOLDEN, f"toy_t{i}.bdelta"))
+    # Int8Tensor::payload_bytes (int8.hpp): values + 4 B row scales instead of 4 B per weight
+    proj = sum(r * c for n, r, c in tensor_shapes(arch) if n.split(".")[-1] in PROJECTIONS)
+    rows = sum(r for n, r, c in tensor_shapes(arch) if n.split(".")[-1] in PROJECTIONS)
+    pool.close_request(rids[0])
+    for r in rids[1:]:
+        pool.close_request(r)
+    assert dense.resident_bytes() - pool.resident_bytes() == 4 * proj - (proj + 4 * rows)
+    pool.close()
+    dense.close()
