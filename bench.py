@@ -140,12 +140,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(inside), "where": where}
 
 
-def algorithmic_bytes(arch, tenants, batch):
-    """2 B per backbone weight + P/8 per distinct tenant (+ activations)."""
+def algorithmic_bytes(arch, tenants, batch, wb=2):
+    """wb B per backbone weight (2 bf16, 1 int8 RTN + 4 B per row scale) + P/8
+    per distinct tenant (+ activations)."""
     d, kv, inter, L = arch["dim"], arch["kv_dim"], arch["intermediate"], arch["n_layers"]
     per_layer = {"qkv": (d + 2 * kv) * d, "o": d * d, "gu": 2 * inter * d, "down": d * inter}
     P = sum(per_layer.values()) * L
-    return {"params": P, "base": 2 * P, "bits": tenants * P / 8, "per_layer": per_layer}
+    rows = (d + 2 * kv + d + 2 * inter + d) * L
+    base = wb * P + (4 * rows if wb == 1 else 0)
+    return {"params": P, "base": base, "bits": tenants * P / 8, "per_layer": per_layer}
 
 
 def kv_bytes(arch, batch, ctx):
@@ -153,7 +156,7 @@ def kv_bytes(arch, batch, ctx):
 
 
 # --------------------------------------------------------------------- ours --
-def build_pool(arch, n_tenants, dev, seed=0, world=1, rank=0):
+def build_pool(arch, n_tenants, dev, seed=0, world=1, rank=0, int8=False):
     import torch
 
     import paper_2402_10193_b200 as bd
@@ -173,7 +176,12 @@ def build_pool(arch, n_tenants, dev, seed=0, world=1, rank=0):
             pool.set_tensor(name, torch.ones(1, c, device=dev))
             continue
         w = (torch.randn(r, c, device=dev, generator=g) * 0.02).to(torch.bfloat16)
-        pool.set_tensor(name, w)
+        if int8 and name.split(".")[-1] in PROJ:  # ServingPool(QuantizedCheckpoint): RTN on the device
+            q, sc = bd.rtn_quantize(w.float())
+            pool.set_tensor_i8(name, q, sc)
+            del q, sc
+        else:
+            pool.set_tensor(name, w)
         if name.split(".")[-1] in PROJ:
             base[name] = w
         del w
@@ -229,7 +237,8 @@ def run_ours(args, rank, world, dev):
     torch.manual_seed(0 if tp else rank)  # tp ranks must see the same activations
     # replicas: every rank its own pool and batch; tp: one row-sharded pool, same seed everywhere
     pool, _, setup_s = build_pool(arch, T, dev, seed=1234 if tp else 1234 + rank,
-                                  world=world if tp else 1, rank=rank if tp else 0)
+                                  world=world if tp else 1, rank=rank if tp else 0,
+                                  int8=args.backbone == "int8")
     rids = [pool.open_request(f"tenant{b % T}") for b in range(B)]
     pos = [0] * B
     x = torch.randn(B, arch["dim"], device=dev)
@@ -301,7 +310,7 @@ def run_ours(args, rank, world, dev):
     tok_s = streams * B / (ms_step / 1e3)
     return dict(ms_step=ms_step, tok_s=tok_s, e2e_ms=e2e_ms, e2e_tok_s=streams * B / (e2e_ms / 1e3),
                 clocks=clk.summary(), kernels_per_step=kernels_per_step, prof=prof, prof_serial=prof_serial,
-                arch=arch, T=T,
+                arch=arch, T=T, wb=1 if args.backbone == "int8" else 2,
                 B=B, ctx=ctx, setup_s=setup_s, launches=bd.launch_count() - launches0,
                 h2d=B * arch["dim"] * 4, d2h=B * arch["dim"] * 4)
 
@@ -324,16 +333,17 @@ def profile_step(pool, reqs, x, y, serial=False):
 
 def roofline(res, hbm_peak, peak_kind):
     """Dominant kernel from the profiled step, with its algorithmic bytes per launch."""
-    arch, T, B = res["arch"], res["T"], res["B"]
+    arch, T, B, wb = res["arch"], res["T"], res["B"], res.get("wb", 2)
     d, kv, inter = arch["dim"], arch["kv_dim"], arch["intermediate"]
     shapes = {"qkv": (d + 2 * kv, d), "o": (d, d), "gu": (2 * inter, d), "down": (d, inter)}
     algo = {}
     for g, (rows, cols) in shapes.items():
-        # K2: weights once + activations + f32 result; K3: every tenant's plane once
-        algo[f"gemm_{g}"] = 2 * rows * cols + 2 * B * cols + 4 * B * rows
+        # K2: weights once (int8: + row scales) + activations + f32 result; K3: every tenant's plane once
+        w = wb * rows * cols + (4 * rows if wb == 1 else 0)
+        algo[f"gemm_{g}"] = w + 2 * B * cols + 4 * B * rows
         algo[f"delta_{g}"] = T * rows * cols / 8 + 2 * B * cols + 4 * B * rows
         # fused K2+K3: the backbone tile and every tenant's plane once
-        algo[f"fused_{g}"] = 2 * rows * cols + T * rows * cols / 8 + 2 * B * cols + 4 * B * rows
+        algo[f"fused_{g}"] = w + T * rows * cols / 8 + 2 * B * cols + 4 * B * rows
     prof = res["prof"]
     cand = {k: v for k, v in prof.items() if k in algo and v["count"]}
     dom = max(cand, key=lambda k: cand[k]["ms"])
@@ -599,7 +609,8 @@ def config_of(args, arch, T, B, ctx):
             "batch_per_gpu": B, "seq_len": ctx,
             "parallelism": (f"tp{args.gpus}" if args.parallelism == "tp" else f"replicas{args.gpus}")
             if args.gpus > 1 else "single",
-            "l2": "working set > L2 (no flush needed)"}
+            "l2": "working set > L2 (no flush needed)",
+            **({"backbone": "int8 RTN (ServingPool(QuantizedCheckpoint))"} if args.backbone == "int8" else {})}
 
 
 # --------------------------------------------------------------- distributed --
@@ -653,6 +664,8 @@ def main():
                     help="N>1: one row-sharded pool over NCCL (north star, strong scaling; default) or "
                          "independent replicas (weak scaling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--backbone", default="bf16", choices=["bf16", "int8"],
+                    help="int8: ServingPool(QuantizedCheckpoint), RTN int8 projections (SURVEY §8(f)#4)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args.gpus))
@@ -696,12 +709,12 @@ def main():
     res = run_ours(args, rank, world, dev)
     hbm, tfl, kind = peaks()
     rl = roofline(res, hbm, kind)
-    byts = algorithmic_bytes(res["arch"], res["T"], res["B"])
+    byts = algorithmic_bytes(res["arch"], res["T"], res["B"], res["wb"])
     line = {"metric": METRIC, "value": round(res["tok_s"], 2), "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(res["ms_step"], 4),
             "higher_is_better": True,
             "scaling": "strong" if (args.parallelism == "tp" and world > 1) else "weak",
-            "vs_baseline": None, "dtype": "bf16",
+            "vs_baseline": None, "dtype": "int8+bf16" if args.backbone == "int8" else "bf16",
             "data": "synthetic (random bf16 backbone; fine = base + N(0,1e-3) compressed on device by K1)",
             "config": config_of(args, res["arch"], res["T"], res["B"], res["ctx"]),
             "e2e": {"value": round(res["e2e_tok_s"], 2), "unit": "tokens/s", "h2d_bytes_per_step": res["h2d"],
