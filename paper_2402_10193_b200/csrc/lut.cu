@@ -216,10 +216,10 @@ __device__ __forceinline__ float lds_imm(uint32_t addr) {
     return v;
 }
 
-__device__ __forceinline__ void build_tables_v2(float* T, const float* xs) {
-    // thread t -> bank t & 31 (c = bank >> 2, b' = bank & 3), word w = (t >> 5) & 3,
+__device__ __forceinline__ void build_tables_v2(float* T, const float* xs, int t) {
+    // builder t < 512 -> bank t & 31 (c = bank >> 2, b' = bank & 3), word w = (t >> 5) & 3,
     // quarter (t >> 7) of the 256 entries; a warp stores one 128-byte row per entry.
-    const int bank = threadIdx.x & 31, w = (threadIdx.x >> 5) & 3, quarter = threadIdx.x >> 7;
+    const int bank = t & 31, w = (t >> 5) & 3, quarter = t >> 7;
     const int col = 128 * (bank >> 2) + 32 * w + 8 * (bank & 3);
     float xv[8];
 #pragma unroll
@@ -275,6 +275,22 @@ __global__ void __maxnreg__(kLutRegs)
     const long long g0 = total * blockIdx.x / gridDim.x;
     const long long g1 = total * (blockIdx.x + 1) / gridDim.x;
     int cur = -1;
+    // x of a unit (request, slice): kXPer values per thread. The next unit's are loaded into
+    // registers right after the current unit's tables are built, so a unit switch does not
+    // wait on global memory.
+    constexpr int kXPer = (kSliceCols + kLutThreads - 1) / kLutThreads;
+    uint16_t xnext[kXPer];
+    int pre = -1;
+    auto load_x = [&](int unit, uint16_t (&v)[kXPer]) {
+        const LutJob& jb = p.jobs[unit / p.slices];
+        const int cb = (unit % p.slices) * kSliceCols;
+        const uint16_t* xr = X + static_cast<size_t>(jb.req) * p.ldx;
+#pragma unroll
+        for (int k = 0; k < kXPer; ++k) {
+            const int i = threadIdx.x + k * kLutThreads;
+            v[k] = (i < kSliceCols && cb + i < p.cols) ? xr[cb + i] : uint16_t(0);
+        }
+    };
     for (long long g = g0; g < g1;) {
         const int u = static_cast<int>(g / p.M);
         const int ra = static_cast<int>(g % p.M);
@@ -283,14 +299,22 @@ __global__ void __maxnreg__(kLutRegs)
         const LutJob& job = p.jobs[job_i];
         const int c0 = slice * kSliceCols;
         if (u != cur) {
+            if (pre != u) load_x(u, xnext);
             __syncthreads();  // previous unit's lookups done
-            const uint16_t* xr = X + static_cast<size_t>(job.req) * p.ldx;
-            for (int i = threadIdx.x; i < kSliceCols; i += kLutThreads)
-                xs[i + (i >> 7)] = (c0 + i < p.cols) ? bf16_to_f32(xr[c0 + i]) : 0.0f;
+#pragma unroll
+            for (int k = 0; k < kXPer; ++k) {
+                const int i = threadIdx.x + k * kLutThreads;
+                if (i < kSliceCols) xs[i + (i >> 7)] = bf16_to_f32(xnext[k]);
+            }
             __syncthreads();
-            build_tables_v2(T, xs);
+            // 512 builders: 128 tables x 4 quarters
+            for (int t = threadIdx.x; t < 512; t += kLutThreads) build_tables_v2(T, xs, t);
             __syncthreads();
             cur = u;
+            if (g - ra + p.M < g1) {  // this CTA's range continues into unit u + 1
+                load_x(u + 1, xnext);
+                pre = u + 1;
+            }
         }
         const bool lane_on = c0 + 128 * chunk < p.cols;
         float* out_u = out + (static_cast<size_t>(slice) * p.batch + job.req) * p.M;
