@@ -147,8 +147,13 @@ struct Plan {
     float** d_lmraw = nullptr;      // [B] or null
     int* d_pos = nullptr;
     int* d_tok = nullptr;
-    int* h_pos = nullptr;           // pinned
-    int* h_tok = nullptr;
+    // pinned staging of positions / tokens, two slots: a slot is rewritten only after the
+    // copy that last read it has run (event), not after the whole previous step, so the host
+    // enqueues step N+1 while step N executes
+    int* h_pos[2] = {nullptr, nullptr};
+    int* h_tok[2] = {nullptr, nullptr};
+    cudaEvent_t staged[2] = {nullptr, nullptr};
+    int slot = 0;
     std::vector<void*> allocs;
     // per layer & group: delta units
     std::vector<std::array<std::vector<DeltaUnit>, 4>> units;  // qkv, o, gu, down
@@ -253,8 +258,11 @@ struct PoolImpl {
             if (p.graph_layers) cudaGraphExecDestroy(p.graph_layers);
             if (p.graph_full) cudaGraphExecDestroy(p.graph_full);
             for (void* q : p.allocs) cudaFree(q);
-            if (p.h_pos) cudaFreeHost(p.h_pos);
-            if (p.h_tok) cudaFreeHost(p.h_tok);
+            for (int k = 0; k < 2; ++k) {
+                if (p.h_pos[k]) cudaFreeHost(p.h_pos[k]);
+                if (p.h_tok[k]) cudaFreeHost(p.h_tok[k]);
+                if (p.staged[k]) cudaEventDestroy(p.staged[k]);
+            }
         }
         plans.clear();
     }
@@ -991,8 +999,11 @@ struct PoolImpl {
         p->d_lmraw = any_lmraw ? upload_ptrs(lmr) : nullptr;
         p->d_pos = dmalloc<int>(B, &p->allocs);
         p->d_tok = dmalloc<int>(B, &p->allocs);
-        BD_CUDA(cudaMallocHost(&p->h_pos, B * sizeof(int)));
-        BD_CUDA(cudaMallocHost(&p->h_tok, B * sizeof(int)));
+        for (int k = 0; k < 2; ++k) {
+            BD_CUDA(cudaMallocHost(&p->h_pos[k], B * sizeof(int)));
+            BD_CUDA(cudaMallocHost(&p->h_tok[k], B * sizeof(int)));
+            BD_CUDA(cudaEventCreateWithFlags(&p->staged[k], cudaEventDisableTiming));
+        }
 
         // tenant segmentation
         std::vector<int> order;
@@ -1435,13 +1446,16 @@ struct PoolImpl {
         // order the pool stream after the caller's stream
         BD_CUDA(cudaEventRecord(ev_in, user));
         BD_CUDA(cudaStreamWaitEvent(stream, ev_in, 0));
-        BD_CUDA(cudaStreamSynchronize(stream));  // pinned staging reuse
+        const int k = p.slot;
+        p.slot ^= 1;
+        BD_CUDA(cudaEventSynchronize(p.staged[k]));  // the copy that last read this slot has run
         for (uint64_t i = 0; i < n; ++i) {
-            p.h_pos[i] = int(reqs[i].position);
-            p.h_tok[i] = reqs[i].token;
+            p.h_pos[k][i] = int(reqs[i].position);
+            p.h_tok[k][i] = reqs[i].token;
         }
-        BD_CUDA(cudaMemcpyAsync(p.d_pos, p.h_pos, n * sizeof(int), cudaMemcpyHostToDevice, stream));
-        BD_CUDA(cudaMemcpyAsync(p.d_tok, p.h_tok, n * sizeof(int), cudaMemcpyHostToDevice, stream));
+        BD_CUDA(cudaMemcpyAsync(p.d_pos, p.h_pos[k], n * sizeof(int), cudaMemcpyHostToDevice, stream));
+        BD_CUDA(cudaMemcpyAsync(p.d_tok, p.h_tok[k], n * sizeof(int), cudaMemcpyHostToDevice, stream));
+        BD_CUDA(cudaEventRecord(p.staged[k], stream));
         if (!full)
             BD_CUDA(cudaMemcpyAsync(x, x_in, n * a.dim * 4, cudaMemcpyDeviceToDevice, stream));
         execute(p, full);

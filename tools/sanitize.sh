@@ -1,0 +1,12 @@
+#!/bin/bash
+# compute-sanitizer (memcheck, racecheck, synccheck) over a small cross-section of the GPU
+# tests: K1 compress, K3 LUT + K2 linear, K6 backward, K2 int8, and the device pool (toy
+# reference tenants, CUDA graph + PDL). Logs -> gpurun_out/sanitize_<tool>.log
+mkdir -p gpurun_out
+SEL="tests/test_gpu_kernels.py::test_compress_golden_f32 tests/test_gpu_kernels.py::test_multitenant_linear_each_delta_path tests/test_gpu_backward.py::test_transpose_accumulate_golden tests/test_gpu_backward.py::test_delta_linear_backward_vs_reference tests/test_gpu_int8.py::test_int8_matmul_nt_vs_reference tests/test_gpu_pool.py::test_shared_matches_reference_logits tests/test_gpu_pool.py::test_int8_backbone_toy_matches_port"
+for tool in memcheck racecheck synccheck; do
+  timeout 1500 compute-sanitizer --tool $tool --target-processes all --print-limit 20 \
+      python -m pytest $SEL -q -x -p no:cacheprovider > gpurun_out/sanitize_$tool.log 2>&1
+  echo "$tool rc=$?" >> gpurun_out/sanitize_summary.txt
+  grep -E "ERROR SUMMARY|RACECHECK SUMMARY|passed|failed" gpurun_out/sanitize_$tool.log | tail -4 >> gpurun_out/sanitize_summary.txt
+done
