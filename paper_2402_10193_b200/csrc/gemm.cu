@@ -24,10 +24,6 @@
 #include "common.cuh"
 #include "kernels.h"
 
-#ifndef BD_K2_ABLATE
-#define BD_K2_ABLATE 0  // experiments: 1 = TMA stream without MMAs, 2 = one stage only
-#endif
-
 namespace bd {
 
 namespace {
@@ -107,11 +103,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // The weights do not depend on the predecessor kernel: the first ring's worth is
         // requested before waiting for it (PDL), the activations only after.
         const uint64_t pol_w = policy_evict_first();  // weights stream once per step
-#if BD_K2_ABLATE == 2
-        const int npre = min(nkb, 1);
-#else
         const int npre = min(nkb, stages);
-#endif
         for (int i = 0; i < npre; ++i) {
             mbar_arrive_expect_tx(&full[i], L.stage_bytes);
             tma_load_2d_hint(smem + i * L.stage_bytes, &map_w, &full[i], (kb0 + i) * (kI8 ? 128 : kBK), m0, pol_w);
@@ -130,9 +122,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 tma_load_2d_hint(a, &map_w, &full[s], kc, m0, pol_w);
             }
             tma_load_2d(b, &map_x, &full[s], kc, 0);
-#if BD_K2_ABLATE == 2
-            break;
-#endif
         }
     } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer ---- (consumes only what the producer's barriers release)
@@ -140,9 +129,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int i = 0; i < nkb; ++i) {
             const int s = i % stages;
             const uint32_t round = i / stages;
-#if BD_K2_ABLATE == 2
-            if (i > 0) break;
-#endif
             mbar_wait(&full[s], round & 1);
             tc_fence_after();
             uint8_t* a = smem + s * L.stage_bytes;
@@ -150,9 +136,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const uint64_t da = sdesc_k128(a), db = sdesc_k128(b);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {  // +32 bytes per K step (16 bf16 / 32 int8)
-#if BD_K2_ABLATE
-                if (i > 0) break;
-#endif
                 if (kI8) mma_i8_ss(taddr, da + 2 * k, db + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
                 else mma_bf16_ss(taddr, da + 2 * k, db + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
             }

@@ -199,6 +199,14 @@ __global__ void __maxnreg__(kLutRegs)
 // Per word: 4 PRMT + 4 LDS + 4 FADD, 1/4 LDG, 1/4 SHFL.
 // Table entry (chunk c, word w, byte b', value e) at byte
 //   65536 (w >> 1) + 256 e + 128 (w & 1) + 4 (4c + b')   (128 KB, same footprint as v1).
+// plane words: read once, never reused by this SM
+__device__ __forceinline__ uint4 ld_plane(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     uint32_t d;
     asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
@@ -334,7 +342,7 @@ __global__ void __maxnreg__(kLutRegs)
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         const int r = min(r0 + 4 * grp + i, lb - 1);
-                        w[i] = __ldcs(plane + static_cast<size_t>(r) * (wpr / 4));
+                        w[i] = ld_plane(plane + static_cast<size_t>(r) * (wpr / 4));
                     }
                 };
                 auto consume = [&](int r0, const uint4 (&wc)[4]) {
@@ -381,8 +389,8 @@ __global__ void __maxnreg__(kLutRegs)
                 // ping-pong register buffers: the next batch's words are in flight while the
                 // current one is looked up (no register moves between iterations)
                 constexpr int kStep = kWarps * kRows;
-                uint4 wa[4], wb[4];
                 int r0 = la + warp * kRows;
+                uint4 wa[4], wb[4];
                 if (r0 < lb) load(r0, wa);
                 while (r0 < lb) {
                     if (r0 + kStep < lb) load(r0 + kStep, wb);
@@ -460,11 +468,7 @@ void lut2_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t s
         // max carveout (K2 co-resident on every SM) where plane rows are 128-B aligned; the
         // down projection (1376-B rows) measured faster on the default carveout, K2 after
         // it (profiles/r02_exp_down_carveout.txt: 1.487 vs 1.857 ms/step for down)
-#ifdef BD_LUT_CARVE_ALL
-        if (true)
-#else
         if (kWPR % 32 == 0 && kWPR > 0)
-#endif
             BD_CUDA(cudaFuncSetAttribute(lut2_kernel<kWPR>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          int(cudaSharedmemCarveoutMaxShared)));
         attr = true;

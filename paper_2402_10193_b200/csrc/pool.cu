@@ -42,6 +42,10 @@
         if (r_ != ncclSuccess) ::bd::fail(BD_ERR_CUDA, std::string(#x) + ": " + ncclGetErrorString(r_)); \
     } while (0)
 
+#ifndef BD_K2_CAP_KB
+#define BD_K2_CAP_KB 88  // K2 beside the LUT: shared memory for its stage ring (KB)
+#endif
+
 namespace bd {
 
 void note_launch();
@@ -1100,7 +1104,7 @@ struct PoolImpl {
             GemmPlan* gs[4] = {&p->g_qkv, &p->g_o, &p->g_gu, &p->g_down};
             for (int gi = 0; gi < 4; ++gi)
                 if (p->lut[0][gi].ok) {
-                    *gs[gi] = plan_gemm(gs[gi]->M, gs[gi]->K, B, 88 * 1024, i8);
+                    *gs[gi] = plan_gemm(gs[gi]->M, gs[gi]->K, B, BD_K2_CAP_KB * 1024, i8);
                     require(uint64_t(gs[gi]->splits) * B * gs[gi]->M <= P_elems, BD_ERR_CUDA,
                             "split-K workspace too small");
                 }
