@@ -67,6 +67,9 @@ __global__ void __launch_bounds__(kQThreads)
     }
 }
 
+// grid (batch, column chunks of 1024): every CTA takes the row maximum over the whole row
+// (16-byte loads, served from L2 after the first CTA) and writes its chunk's pieces
+constexpr int kQChunk = 1024;
 __global__ void __launch_bounds__(kQThreads)
     quant_pieces_kernel(const void* __restrict__ X, int x_f32, int ldx, int K, int8_t* __restrict__ Xq, int ldq,
                         float* __restrict__ piece_scale) {
@@ -79,7 +82,20 @@ __global__ void __launch_bounds__(kQThreads)
     };
     griddep_wait();  // PDL: X comes from the previous kernel
     float m = 0.0f;
-    for (int k = threadIdx.x; k < K; k += kQThreads) m = fmaxf(m, fabsf(load(k)));
+    if (!x_f32 && ldx % 8 == 0) {
+        const uint4* row = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(X) + size_t(b) * ldx);
+        for (int k8 = threadIdx.x; k8 * 8 < K; k8 += kQThreads) {
+            const uint4 u = row[k8];
+            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+                const float v = __uint_as_float((h & 1 ? w[h >> 1] & 0xFFFF0000u : w[h >> 1] << 16));
+                if (k8 * 8 + h < K) m = fmaxf(m, fabsf(v));
+            }
+        }
+    } else {
+        for (int k = threadIdx.x; k < K; k += kQThreads) m = fmaxf(m, fabsf(load(k)));
+    }
     m = block_max(m, red);
     int S = 0;
     if (m > 0.0f) {
@@ -87,10 +103,11 @@ __global__ void __launch_bounds__(kQThreads)
         frexpf(m, &e);  // m = f 2^e, f in [0.5, 1)
         S = 6 - e;      // m 2^S in [32, 64)
     }
-    if (threadIdx.x < kPieces)
+    if (blockIdx.y == 0 && threadIdx.x < kPieces)
         piece_scale[b * kPieces + threadIdx.x] = m > 0.0f ? ldexpf(1.0f, -(S + 7 * int(threadIdx.x))) : 0.0f;
     int8_t* q0 = Xq + size_t(b) * kPieces * ldq;
-    for (int k = threadIdx.x; k < ldq; k += kQThreads) {
+    const int k_end = min(ldq, int(blockIdx.y + 1) * kQChunk);
+    for (int k = blockIdx.y * kQChunk + threadIdx.x; k < k_end; k += kQThreads) {
         float v = m > 0.0f ? ldexpf(load(k), S) : 0.0f;
 #pragma unroll
         for (int p = 0; p < kPieces; ++p) {
@@ -126,8 +143,8 @@ void quant_pieces_launch(const void* X, bool x_f32, int ldx, int K, int batch, i
                          float* piece_scale, cudaStream_t stream) {
     require(ldq >= K && ldq % 16 == 0, BD_ERR_BAD_ARGUMENT, "int8 pieces: bad row stride");
     if (batch <= 0) return;
-    BD_CUDA(launch_pdl(quant_pieces_kernel, dim3(batch), dim3(kQThreads), 0, stream, X, x_f32 ? 1 : 0, ldx, K,
-                       Xq, ldq, piece_scale));
+    BD_CUDA(launch_pdl(quant_pieces_kernel, dim3(batch, (ldq + kQChunk - 1) / kQChunk), dim3(kQThreads), 0, stream,
+                       X, x_f32 ? 1 : 0, ldx, K, Xq, ldq, piece_scale));
     note_launch();
     BD_CUDA(cudaGetLastError());
 }
