@@ -8,8 +8,9 @@
 //      u_pl = the forward's S_pl x (LinearTape::plane_u).
 //
 // (1) Each thread owns 32 consecutive columns (one 32-bit window of a row's bits, any
-//     bit offset: rows need not start on a byte) and walks a chunk of rows, adding +-y_i
-//     into 32 fp64 accumulators (the reference keeps its column sums in double too);
+//     bit offset: rows need not start on a byte) and walks a chunk of rows (8 row words in
+//     flight), adding +-y_i into 32 fp64 accumulators (the reference keeps its column sums
+//     in double too); chunks are sized so the grid is ~4 CTAs per SM;
 //     chunk partials [chunk][vec][col] are summed in chunk order by a second kernel and
 //     rounded to f32 once (deterministic, no atomics). HBM: the plane is read once per
 //     vector, rows * cols / 8 bytes.
@@ -27,7 +28,7 @@ void note_launch();
 namespace {
 
 constexpr int kTtThreads = 128;     // 128 x 32 = 4096 columns per block
-constexpr int kTtRows = 64;         // rows per chunk
+constexpr int kTtBlocks = 4 * kNumSMs;  // target grid: row chunks sized so the grid fills the GPU
 
 __device__ __forceinline__ uint32_t window32(const uint8_t* __restrict__ bits, uint64_t nbytes,
                                              uint64_t pos, bool aligned) {
@@ -40,15 +41,14 @@ __device__ __forceinline__ uint32_t window32(const uint8_t* __restrict__ bits, u
     return static_cast<uint32_t>(v >> (pos & 7));
 }
 
-// grid (column blocks, row chunks, vectors); part[(chunk * n_vec + v) * cols + j]
+// grid (column blocks, row chunks of chunk_rows, vectors); part[(chunk * n_vec + v) * cols + j]
 __global__ void __launch_bounds__(kTtThreads)
     transpose_acc_kernel(const uint8_t* __restrict__ bits, uint64_t rows, uint64_t cols,
-                         const float* __restrict__ y, uint64_t n_vec, double* __restrict__ part) {
-    __shared__ float ys[kTtRows];
+                         const float* __restrict__ y, uint64_t n_vec, uint64_t chunk_rows,
+                         double* __restrict__ part) {
     const uint64_t v = blockIdx.z, chunk = blockIdx.y;
-    const uint64_t r0 = chunk * kTtRows, r1 = min(rows, r0 + kTtRows);
-    for (uint64_t r = r0 + threadIdx.x; r < r1; r += kTtThreads) ys[r - r0] = y[v * rows + r];
-    __syncthreads();
+    const uint64_t r0 = chunk * chunk_rows, r1 = min(rows, r0 + chunk_rows);
+    const float* yv = y + v * rows;
     const uint64_t c0 = (uint64_t(blockIdx.x) * kTtThreads + threadIdx.x) * 32;
     if (c0 >= cols) return;
     const int take = cols - c0 < 32 ? int(cols - c0) : 32;
@@ -57,11 +57,19 @@ __global__ void __launch_bounds__(kTtThreads)
     double acc[32];
 #pragma unroll
     for (int k = 0; k < 32; ++k) acc[k] = 0.0;
-    for (uint64_t r = r0; r < r1; ++r) {
-        const double yr = ys[r - r0];
-        const uint32_t w = window32(bits, nbytes, r * cols + c0, aligned);
+    // 8 row words in flight per batch (the row loop is otherwise one dependent load per row)
+    for (uint64_t rb = r0; rb < r1; rb += 8) {
+        uint32_t w[8];
 #pragma unroll
-        for (int k = 0; k < 32; ++k) acc[k] += ((w >> k) & 1u) ? yr : -yr;
+        for (int i = 0; i < 8; ++i)
+            w[i] = rb + i < r1 ? window32(bits, nbytes, (rb + i) * cols + c0, aligned) : 0u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (rb + i >= r1) break;
+            const double yr = __ldg(yv + rb + i);  // one address per warp: broadcast
+#pragma unroll
+            for (int k = 0; k < 32; ++k) acc[k] += ((w[i] >> k) & 1u) ? yr : -yr;
+        }
     }
     double* out = part + (chunk * n_vec + v) * cols + c0;
 #pragma unroll
@@ -76,7 +84,16 @@ __global__ void transpose_reduce_kernel(const double* __restrict__ part, uint64_
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n_vec * cols) return;
     double s = 0.0;
-    for (uint64_t c = 0; c < n_chunks; ++c) s += part[c * n_vec * cols + i];
+    const uint64_t stride = n_vec * cols;
+    uint64_t c = 0;
+    for (; c + 8 <= n_chunks; c += 8) {  // 8 loads in flight, added in chunk order
+        double t[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t[k] = part[(c + k) * stride + i];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s += t[k];
+    }
+    for (; c < n_chunks; ++c) s += part[c * stride + i];
     const float col = static_cast<float>(s);
     out[i] = overwrite ? scale * col : out[i] + scale * col;
 }
@@ -119,13 +136,18 @@ void packed_transpose_launch(const uint8_t* bits, uint64_t rows, uint64_t cols, 
         return;
     }
     require(n_vec <= 65535, BD_ERR_BAD_ARGUMENT, "packed_signed_accumulate_t: too many vectors");
-    const uint64_t n_chunks = (rows + kTtRows - 1) / kTtRows;
-    require(n_chunks <= 65535, BD_ERR_BAD_ARGUMENT, "packed_signed_accumulate_t: too many rows");
+    const uint64_t col_blocks = (cols + 32ull * kTtThreads - 1) / (32ull * kTtThreads);
+    // enough row chunks to fill the GPU, and no more: the fp64 partials are chunks x vectors x cols
+    const uint64_t want = std::max<uint64_t>(1, kTtBlocks / (col_blocks * n_vec));
+    uint64_t chunk_rows = (rows + want - 1) / want;
+    chunk_rows = std::max<uint64_t>(64, (chunk_rows + 7) / 8 * 8);  // >= 64: bounded partial sums
+    const uint64_t n_chunks = (rows + chunk_rows - 1) / chunk_rows;
+    require(n_chunks <= 65535 && col_blocks <= 0x7fffffffull, BD_ERR_BAD_ARGUMENT,
+            "packed_signed_accumulate_t: shape too large");
     double* part = nullptr;
     BD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), n_chunks * n_vec * cols * sizeof(double), s));
-    const dim3 grid(unsigned((cols + 32ull * kTtThreads - 1) / (32ull * kTtThreads)), unsigned(n_chunks),
-                    unsigned(n_vec));
-    transpose_acc_kernel<<<grid, kTtThreads, 0, s>>>(bits, rows, cols, y, n_vec, part);
+    const dim3 grid{unsigned(col_blocks), unsigned(n_chunks), unsigned(n_vec)};
+    transpose_acc_kernel<<<grid, kTtThreads, 0, s>>>(bits, rows, cols, y, n_vec, chunk_rows, part);
     note_launch();
     BD_CUDA(cudaGetLastError());
     const uint64_t n = n_vec * cols;
