@@ -235,6 +235,69 @@ __global__ void __launch_bounds__(kRnThreads)
     if (threadIdx.x == 0) trace_rec(TR_NORM, t_entry, t_wait);
 }
 
+// The same with the CTAs of a request as one thread-block cluster (dim <= 8 x kRnChunk): the
+// chunk sums of squares meet in distributed shared memory behind a cluster barrier instead of
+// a global arrival counter (same addition order -> same bits).
+__global__ void __launch_bounds__(kRnThreads)
+    resid_norm_cluster_kernel(float* __restrict__ x, int dim, ProjOut proj, const float* const* __restrict__ norm_w,
+                              uint16_t* __restrict__ xn, int ldxn, float* __restrict__ xn_f32) {
+    __shared__ double red_d[32];
+    __shared__ double part_sq;
+    __shared__ double inv_s;
+    const unsigned long long t_entry = gtimer();
+    griddep_wait();  // PDL: the projection partials come from the previous kernel
+    const unsigned long long t_wait = gtimer();
+    const int b = blockIdx.y, nc = gridDim.x;
+    const int i = blockIdx.x * kRnChunk + 4 * threadIdx.x;
+    const bool on = i < dim;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    float* xb = x + size_t(b) * dim;
+    if (on) {
+        v = *reinterpret_cast<const float4*>(xb + i);
+        if (proj.P || proj.G) {
+            v = f4_add(v, proj_val4(proj, b, proj.col0 + i));
+            *reinterpret_cast<float4*>(xb + i) = v;
+        }
+    }
+    const float4 w = on ? *reinterpret_cast<const float4*>(norm_w[b] + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    double sq = static_cast<double>(v.x) * v.x + static_cast<double>(v.y) * v.y +
+                static_cast<double>(v.z) * v.z + static_cast<double>(v.w) * v.w;
+    sq = block_sum(sq, red_d);
+    if (threadIdx.x == 0) part_sq = sq;
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (threadIdx.x == 0) {
+        double msq = 0.0;
+        const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(&part_sq));
+        for (int k = 0; k < nc; ++k) {
+            uint32_t remote;
+            double pk;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(k));
+            asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(pk) : "r"(remote) : "memory");
+            msq += pk;
+        }
+        inv_s = 1.0 / sqrt(msq / static_cast<double>(dim) + 1e-12);
+    }
+    // no CTA leaves (its part_sq must stay readable) before every CTA has read the sums
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    (void)rank;
+    if (!on) return;
+    const double inv = inv_s;
+    const float y0 = static_cast<float>(static_cast<double>(v.x) * inv) * w.x;
+    const float y1 = static_cast<float>(static_cast<double>(v.y) * inv) * w.y;
+    const float y2 = static_cast<float>(static_cast<double>(v.z) * inv) * w.z;
+    const float y3 = static_cast<float>(static_cast<double>(v.w) * inv) * w.w;
+    if (xn) {
+        uint2 pk;
+        pk.x = uint32_t(f32_to_bf16(y0)) | (uint32_t(f32_to_bf16(y1)) << 16);
+        pk.y = uint32_t(f32_to_bf16(y2)) | (uint32_t(f32_to_bf16(y3)) << 16);
+        *reinterpret_cast<uint2*>(xn + size_t(b) * ldxn + i) = pk;
+    }
+    if (xn_f32) *reinterpret_cast<float4*>(xn_f32 + size_t(b) * dim + i) = make_float4(y0, y1, y2, y3);
+    if (threadIdx.x == 0) trace_rec(TR_NORM, t_entry, t_wait);
+}
+
 // one block per (head, request): RoPE, KV append, scores, softmax, context
 __global__ void attn_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos_dev,
                             uint16_t* __restrict__ ctx_out, int ld_ctx) {
@@ -705,6 +768,13 @@ void resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const 
     // one-launch path: the CTAs of a request meet on an arrival counter, so the whole
     // grid must be co-resident (<= 8 CTAs per SM here) -> bounded grid size
     const int nc = (dim + kRnChunk - 1) / kRnChunk;
+    if (norm_w && dim % 4 == 0 && ldxn % 4 == 0 && proj_vec4_ok(proj) && nc >= 2 && nc <= 8) {
+        BD_CUDA(launch_pdl_cluster(resid_norm_cluster_kernel, dim3(nc, batch), dim3(kRnThreads), 0, s, unsigned(nc),
+                                   x, dim, proj, norm_w, xn, ldxn, xn_f32));
+        note_launch();
+        BD_CUDA(cudaGetLastError());
+        return;
+    }
     if (dim % 4 == 0 && ldxn % 4 == 0 && proj_vec4_ok(proj) &&
         size_t(nc) * batch <= size_t(kNumSMs) * 8) {
         BD_CUDA(launch_pdl(resid_norm_kernel, dim3(nc, batch), dim3(kRnThreads), 0, s, x, dim, proj, norm_w, xn,
