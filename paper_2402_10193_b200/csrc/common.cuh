@@ -171,27 +171,6 @@ __host__ __device__ constexpr uint32_t idesc_s8s8_s32(uint32_t M, uint32_t N) {
     return (2u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
-// ---- FP4 (e2m1) sign planes on the tensor cores (K23 mt4.cu, K3m mxd.cu) ----
-// kind::mxf4 instruction descriptor: A = B = E2M1 (1), scale type UE8M0, K = 64
-__host__ __device__ constexpr uint32_t idesc_mxf4(uint32_t M, uint32_t N) {
-    return (1u << 7) | (1u << 10) | ((N >> 3) << 17) | (1u << 23) | ((M >> 4) << 24);
-}
-// 128-byte-swizzled K-major tile, 8-row groups `sbo` bytes apart
-__device__ __forceinline__ uint64_t sdesc_sw128(const void* smem, uint32_t sbo) {
-    const uint64_t addr = smem_u32(smem);
-    return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) |
-           (2ull << 61);
-}
-__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&r)[4]) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
-                 "r"(r[2]), "r"(r[3])
-                 : "memory");
-}
-// bit 4i+c of a plane word -> nibble i of register c: 0x2 = +1.0 (bit 1), 0xA = -1.0 (bit 0)
-__device__ __forceinline__ uint32_t expand4(uint32_t w, int c) {
-    return ((w << (3 - c)) & 0x88888888u) ^ 0xAAAAAAAAu;
-}
-
 // Shared-memory matrix descriptor for a K-major tile written by TMA with
 // 128-byte swizzle: rows of 128 B, 8-row (1024 B) swizzle atoms.
 //   [0,14) start>>4 | [16,30) LBO>>4 (unused for swizzled K-major, =1) |

@@ -151,22 +151,6 @@ bool plan_lut(LutParams& p, const int* seg_rows, int n_segs, int cols, int ldx, 
 // out: [slices][batch][M] f32, alpha already applied; every (slice, req, row) of a job written
 void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream);
 
-// ---- K3m: tenant deltas on the FP4 tensor cores beside K2 (mxd.cu) ----
-// one request per job, one plane per projection; output D[req][m] over the full K (dsplits 1)
-struct MxdParams {
-    int n_jobs, n_segs, M, K, n_chunks, tiles, n_tasks, grid;
-    int seg_row0[kLutMaxSegs + 1];
-    const CUtensorMap* maps;  // device [job][seg] plane maps (tmap_bits4)
-    const uint8_t* xpk;       // FP4 activation pieces (xp_prep_launch)
-    float* out;               // D [batch][M]
-    int req[kLutMaxJobs];
-    float alpha[kLutMaxJobs][kLutMaxSegs];
-};
-// From a planned LUT job list (lp: plan_lut done); false if unsupported. Host maps -> upload
-// and set p.maps, set p.xpk and p.out.
-bool plan_mxd(MxdParams& p, const LutParams& lp, const std::vector<int>& seg_rows, std::vector<CUtensorMap>& maps);
-void mxd_launch(const MxdParams& p, cudaStream_t stream);
-
 // ---- K5: fp32 multi-tenant linear (SIMT, fp64 accumulation; packed.cu) ----
 // Y[b] = W x_b + alpha_b S_b x_b for every b < batch (req_bits[b] == null: base only);
 // W f32 [rows x cols], X f32 [batch x cols], Y f32 [batch x rows]

@@ -97,12 +97,26 @@ __device__ __forceinline__ void mma_mxf4_ts(uint32_t d, uint32_t a, uint64_t bde
         : "memory");
 }
 
+// kind::mxf4 instruction descriptor: A = B = E2M1 (1), scale type UE8M0, K = 64
+__host__ __device__ constexpr uint32_t idesc_mxf4(uint32_t M, uint32_t N) {
+    return (1u << 7) | (1u << 10) | ((N >> 3) << 17) | (1u << 23) | ((M >> 4) << 24);
+}
 
 __device__ __forceinline__ int cta_of(long long s, long long total, int grid) {
     return static_cast<int>(((s + 1) * grid + total - 1) / total) - 1;
 }
 
+__device__ __forceinline__ uint64_t sdesc_sw128(const void* smem, uint32_t sbo) {
+    const uint64_t addr = smem_u32(smem);
+    return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) |
+           (2ull << 61);
+}
 
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&r)[4]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
+                 "r"(r[2]), "r"(r[3])
+                 : "memory");
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
@@ -112,6 +126,9 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
         : "memory");
 }
 
+__device__ __forceinline__ uint32_t expand4(uint32_t w, int c) {
+    return ((w << (3 - c)) & 0x88888888u) ^ 0xAAAAAAAAu;
+}
 
 
 // Stage cursor over a per-tile schedule table (built on the host, kept in smem).

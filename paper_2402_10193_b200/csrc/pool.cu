@@ -178,12 +178,6 @@ struct Plan {
         Mt4Params prm;
     };
     std::vector<std::array<M4, 4>> mt4;
-    // K3m (FP4 tensor-core deltas beside K2) per layer & group
-    struct Mx {
-        bool ok = false;
-        MxdParams prm;
-    };
-    std::vector<std::array<Mx, 4>> mxd;
     uint8_t* xpk = nullptr;  // FP4 activation pieces + scales [B][chunks][kXpBlock]
     cudaGraphExec_t graph_layers = nullptr, graph_full = nullptr;
     uint64_t kernels_layers = 0, kernels_full = 0;
@@ -862,39 +856,6 @@ struct PoolImpl {
         }
     }
 
-    // K3m (mxd.cu) from the LUT plan: same jobs, FP4 tensor cores instead of byte tables
-    void plan_mxd_groups(Plan& p) {
-        const uint64_t nL = a.n_layers;
-        p.mxd.assign(nL, {});
-        const int max_chunks = xp_chunks(int(std::max(a.dim, a.intermediate)));
-        for (int gi = 0; gi < 4; ++gi) {
-            bool ok = p.lut.size() == nL;
-            for (uint64_t l = 0; l < nL && ok; ++l) {
-                const auto& lp = p.lut[l][gi];
-                if (!lp.ok || lp.prm.size() != 1) { ok = false; break; }
-                std::vector<int> seg_rows;
-                for (int sg = 0; sg < lp.prm[0].n_segs; ++sg)
-                    seg_rows.push_back(lp.prm[0].seg_row0[sg + 1] - lp.prm[0].seg_row0[sg]);
-                std::vector<CUtensorMap> maps;
-                MxdParams m;
-                if (!plan_mxd(m, lp.prm[0], seg_rows, maps)) { ok = false; break; }
-                CUtensorMap* dm = dmalloc<CUtensorMap>(maps.size(), &p.allocs);
-                BD_CUDA(cudaMemcpy(dm, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
-                if (!p.xpk) {
-                    p.xpk = dmalloc<uint8_t>(size_t(p.B) * max_chunks * kXpBlock, &p.allocs);
-                    BD_CUDA(cudaMemset(p.xpk, 0, size_t(p.B) * max_chunks * kXpBlock));
-                }
-                m.maps = dm;
-                m.xpk = p.xpk;
-                m.out = D;
-                p.mxd[l][gi].prm = m;
-                p.mxd[l][gi].ok = true;
-            }
-            if (!ok)
-                for (uint64_t l = 0; l < nL; ++l) p.mxd[l][gi].ok = false;
-        }
-    }
-
     // K23 (mt4.cu): base GEMM + every tenant plane as FP4 MMAs in one persistent
     // kernel. Slots are ordered by tenant id and, within a tenant, by request id,
     // so the schedule (and every output bit) is independent of the batch order.
@@ -1132,8 +1093,7 @@ struct PoolImpl {
         // K23 fuses the bf16 base GEMM: not for an int8 backbone
         if (!i8 && (delta_mode == "mt4" || (delta_mode == "auto" && mean_per_tenant >= k23_min_requests(B))))
             plan_mt4_groups(*p, by_t);
-        if (delta_mode == "lut" || delta_mode == "auto" || delta_mode == "mxd") plan_lut_groups(*p);
-        if (delta_mode == "mxd") plan_mxd_groups(*p);
+        if (delta_mode == "lut" || delta_mode == "auto") plan_lut_groups(*p);
         // groups already served by K23 keep no LUT plan
         for (uint64_t l = 0; l < p->mt4.size(); ++l)
             for (int gi = 0; gi < 4; ++gi)
@@ -1187,7 +1147,6 @@ struct PoolImpl {
 
     bool lut_ok(const Plan& p, uint64_t l, int gi) const { return p.lut.size() > l && p.lut[l][gi].ok; }
     bool mt4_ok(const Plan& p, uint64_t l, int gi) const { return p.mt4.size() > l && p.mt4[l][gi].ok; }
-    bool mxd_ok(const Plan& p, uint64_t l, int gi) const { return p.mxd.size() > l && p.mxd[l][gi].ok; }
     ProjOut group_out(const Plan& p, uint64_t l, int gi, const GemmPlan& g) const {
         if (mt4_ok(p, l, gi)) {
             const Mt4Params& f = p.mt4[l][gi].prm;
@@ -1199,7 +1158,6 @@ struct PoolImpl {
             o.M = f.M;
             return o;
         }
-        if (mxd_ok(p, l, gi)) return proj_out(g, true);  // one full-K delta partial
         if (lut_ok(p, l, gi)) {
             ProjOut o = proj_out(g, true);
             o.dsplits = p.lut[l][gi].prm[0].slices;
@@ -1229,23 +1187,6 @@ struct PoolImpl {
         if (mt4_ok(p, l, group)) {
             prof(BD_PROF_XQ_PREP, s, [&] { xp_prep_launch(X, ldx, cols, B, p.xpk, s); });
             prof(BD_PROF_FUSED_QKV + group, s, [&] { mt4_launch(p.mt4[l][group].prm, s); });
-            return;
-        }
-        if (mxd_ok(p, l, group)) {
-            prof(BD_PROF_XQ_PREP, s, [&] { xp_prep_launch(X, ldx, cols, B, p.xpk, s); });
-            if (!concurrent_k23) {  // serial profile: K2 and K3m timed on their own
-                prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm(g, l, group, mw, mx, s); });
-                prof(BD_PROF_DELTA_QKV + group, s, [&] { mxd_launch(p.mxd[l][group].prm, s); });
-                return;
-            }
-            prof(BD_PROF_FUSED_QKV + group, s, [&] {
-                BD_CUDA(cudaEventRecord(ev_fork, s));
-                BD_CUDA(cudaStreamWaitEvent(stream2, ev_fork, 0));
-                mxd_launch(p.mxd[l][group].prm, s);
-                base_gemm(g, l, group, mw, mx, stream2);
-                BD_CUDA(cudaEventRecord(ev_join, stream2));
-                BD_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
-            });
             return;
         }
         if (lut_ok(p, l, group)) {
@@ -1388,7 +1329,6 @@ struct PoolImpl {
             char c = 'U';
             if (a.n_layers == 0) c = '-';
             else if (mt4_ok(p, 0, gi)) c = 'T';
-            else if (mxd_ok(p, 0, gi)) c = 'M';
             else if (lut_ok(p, 0, gi)) c = 'L';
             stats.delta_paths[gi] = c;
         }

@@ -170,15 +170,3 @@ def test_int8_backbone_m7_gqa_B64_T16(cuda, port):
     """int8 backbone at batch 64 (256 MMA columns of pieces), GQA, 4 requests per tenant: the
     LUT (K23 fuses a bf16 GEMM and is not planned for an int8 backbone)."""
     assert run_config(port, dict(M7, n_layers=1), 16, 64, steps=1, expect_paths="LLLL", int8=True) <= 1e-2
-
-
-@pytest.mark.parametrize("arch,n_layers,tenants,batch,paths", [
-    (L7, 1, 8, 8, "MMMM"),      # configs[1]
-    (L7, 2, 16, 16, "MMMM"),    # configs[2] shape, 2 layers
-    (M7, 1, 64, 64, "MMMM"),    # GQA, 64 tenants
-])
-def test_k3m_tensor_core_deltas(cuda, port, monkeypatch, arch, n_layers, tenants, batch, paths):
-    """K3m (mxd.cu): the tenant deltas as kind::mxf4 MMAs against FP4 pieces of the
-    activations, beside K2, against the oracle."""
-    monkeypatch.setenv("BD_DELTA", "mxd")
-    assert run_config(port, dict(arch, n_layers=n_layers), tenants, batch, steps=2, expect_paths=paths) <= 1e-2
