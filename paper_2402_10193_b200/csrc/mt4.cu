@@ -519,6 +519,12 @@ __device__ __forceinline__ float e2m1_value(uint32_t c) {
     return c < 4 ? 0.5f * c : static_cast<float>(c - 2);
 }
 
+// v * 2^k, exact (a multiply by a constructed power of two in the normal exponent range)
+__device__ __forceinline__ float mul_pow2(float v, int k) {
+    if (k >= -126 && k <= 127) return v * __int_as_float((k + 127) << 23);
+    return ldexpf(v, k);
+}
+
 __global__ void __launch_bounds__(256) xp_prep_kernel(const uint16_t* __restrict__ X, int ldx, int K, int n_chunks,
                                                        uint8_t* __restrict__ xpk) {
     __shared__ uint32_t nib[8][32];
@@ -537,19 +543,21 @@ __global__ void __launch_bounds__(256) xp_prep_kernel(const uint16_t* __restrict
         frexpf(amax, &e);  // amax <= 2^e
         E = e - 2;         // amax / 2^E <= 4
     }
+    // f32 is exact here: x is bf16 (8 significant bits), every piece value has <= 2 and the
+    // scalings are powers of two, so r keeps <= 8 significant bits (no rounding anywhere)
     uint32_t packed = 0;
-    double r = x;
+    float r = x;
     uint32_t sbyte[8];
 #pragma unroll
     for (int pc = 0; pc < 8; ++pc) {
         const int s = E - 3 * pc;
         uint32_t code = 0;
         if (amax > 0.0f && s >= -127) {
-            const double v = ldexp(r, -s);
-            code = e2m1_code(static_cast<float>(fabs(v)));
-            const double qv = (v < 0 ? -1.0 : 1.0) * e2m1_value(code);
-            r -= ldexp(qv, s);
-            if (v < 0 && code) code |= 8u;
+            const float v = mul_pow2(r, -s);
+            code = e2m1_code(fabsf(v));
+            const float qv = v < 0.0f ? -e2m1_value(code) : e2m1_value(code);
+            r -= mul_pow2(qv, s);
+            if (v < 0.0f && code) code |= 8u;
         }
         packed |= code << (4 * pc);
         sbyte[pc] = static_cast<uint32_t>(s >= -127 ? s + 127 : 0);
