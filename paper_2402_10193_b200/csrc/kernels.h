@@ -151,6 +151,40 @@ bool plan_lut(LutParams& p, const int* seg_rows, int n_segs, int cols, int ldx, 
 // out: [slices][batch][M] f32, alpha already applied; every (slice, req, row) of a job written
 void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream);
 
+// ---- K3d: tenants with many requests, dense tensor-core delta (mtd.cu) ----
+constexpr int kMtdMaxTenants = 8;
+constexpr int kMtdMaxN = 64;  // requests per tenant (MMA N, padded to 16)
+struct MtdTenant {
+    std::vector<int> reqs;  // batch indices
+    int n_planes[kLutMaxSegs];
+    const uint8_t* bits[kLutMaxSegs];
+    float alpha[kLutMaxSegs];
+};
+struct MtdGather {
+    int rows;
+    int n_req[kMtdMaxTenants], n_pad[kMtdMaxTenants], row0[kMtdMaxTenants];
+    int req[kMtdMaxTenants][kMtdMaxN];
+};
+struct MtdParams {
+    int n_tasks, tiles, M, K, n_segs, n_ten, x_rows, grid;
+    int n_chunks, ksplit, chunks_per_split;  // 256-column chunks; K splits (delta partials)
+    size_t dstride;                          // elements between delta partials (batch x M)
+    int seg_row0[kLutMaxSegs + 1];
+    const CUtensorMap* plane_maps;  // device [tenant][seg]: box [128 rows x 32 B]
+    const CUtensorMap* x_maps;      // device [tenant]: gathered X rows, box [n_pad rows x 64 cols]
+    float* out;                     // D [batch][M]
+    int n_req[kMtdMaxTenants], n_pad[kMtdMaxTenants], x_row0[kMtdMaxTenants];
+    int req[kMtdMaxTenants][kMtdMaxN];
+    float alpha[kMtdMaxTenants][kLutMaxSegs];
+};
+// false if unsupported (K % 256, tenant / request counts, one plane per projection)
+bool plan_mtd(MtdParams& p, MtdGather& g, const std::vector<MtdTenant>& tens, const int* seg_rows, int n_segs,
+              int K, int ldx, int max_splits, std::vector<CUtensorMap>& plane_maps);
+std::vector<CUtensorMap> mtd_x_maps(const MtdParams& p, const void* Xp, int ldp);
+void mtd_gather_launch(const void* X, int ldx, int K, const MtdGather& g, int n_ten, void* Xp, int ldp,
+                       cudaStream_t stream);
+void mtd_launch(const MtdParams& p, cudaStream_t stream);
+
 // ---- K5: fp32 multi-tenant linear (SIMT, fp64 accumulation; packed.cu) ----
 // Y[b] = W x_b + alpha_b S_b x_b for every b < batch (req_bits[b] == null: base only);
 // W f32 [rows x cols], X f32 [batch x cols], Y f32 [batch x rows]

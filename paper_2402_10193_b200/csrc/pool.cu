@@ -178,6 +178,15 @@ struct Plan {
         Mt4Params prm;
     };
     std::vector<std::array<M4, 4>> mt4;
+    // K3d (tenants with many requests: one dense tensor-core delta per tenant) per layer & group
+    struct Md {
+        bool ok = false;
+        MtdParams prm;
+        MtdGather gat;
+    };
+    std::vector<std::array<Md, 4>> mtd;
+    uint16_t* xg = nullptr;  // gathered activations (tenant-major, padded), K3d only
+    int xg_ld = 0;
     uint8_t* xpk = nullptr;  // FP4 activation pieces + scales [B][chunks][kXpBlock]
     cudaGraphExec_t graph_layers = nullptr, graph_full = nullptr;
     uint64_t kernels_layers = 0, kernels_full = 0;
@@ -856,6 +865,74 @@ struct PoolImpl {
         }
     }
 
+    // K3d (mtd.cu): per tenant Y_t = alpha_t S_t X_t^T on the tensor cores, the tenant's
+    // requests as the MMA's N (ascending pool request id inside a tenant, tenants by id)
+    void plan_mtd_groups(Plan& p, std::map<int, std::vector<int>>& by_t) {
+        const uint64_t nL = a.n_layers;
+        p.mtd.assign(nL, {});
+        struct GroupDef {
+            std::vector<int> projs;
+            uint64_t cols, ldx;
+        };
+        const GroupDef defs[4] = {{{P_Q, P_K, P_V}, a.dim, ld_dim},
+                                  {{P_O}, a.dim, ld_dim},
+                                  {{P_GATE, P_UP}, a.dim, ld_dim},
+                                  {{P_DOWN}, a.intermediate, ld_inter}};
+        for (int gi = 0; gi < 4; ++gi) {
+            const GroupDef& gd = defs[gi];
+            int seg_rows[kLutMaxSegs];
+            for (size_t s2 = 0; s2 < gd.projs.size(); ++s2) {
+                uint64_t r0, nr;
+                local_rows(gd.projs[s2], r0, nr);
+                seg_rows[s2] = int(nr);
+            }
+            bool ok = true;
+            for (uint64_t l = 0; l < nL && ok; ++l) {
+                std::vector<MtdTenant> tens;
+                for (auto& kv : by_t) {
+                    MtdTenant mt{};
+                    mt.reqs = kv.second;
+                    std::sort(mt.reqs.begin(), mt.reqs.end(), [&](int x, int y) { return p.reqs[x] < p.reqs[y]; });
+                    for (size_t s2 = 0; s2 < gd.projs.size(); ++s2) {
+                        const auto& planes = tenants[kv.first].proj[l][gd.projs[s2]];
+                        mt.n_planes[s2] = int(planes.size());
+                        mt.bits[s2] = planes.empty() ? nullptr : planes[0].bits;
+                        mt.alpha[s2] = planes.empty() ? 0.0f : planes[0].alpha;
+                    }
+                    tens.push_back(mt);
+                }
+                std::vector<CUtensorMap> pmaps;
+                Plan::Md md;
+                int M = 0;
+                for (size_t s2 = 0; s2 < gd.projs.size(); ++s2) M += seg_rows[s2];
+                const int max_splits = int(D_elems / (size_t(p.B) * size_t(M)));
+                if (!plan_mtd(md.prm, md.gat, tens, seg_rows, int(gd.projs.size()), int(gd.cols), int(gd.ldx),
+                              max_splits, pmaps)) {
+                    ok = false;
+                    break;
+                }
+                md.prm.dstride = size_t(p.B) * size_t(M);
+                if (!p.xg) {
+                    p.xg_ld = int(std::max(ld_dim, ld_inter));
+                    p.xg = dmalloc<uint16_t>(size_t(md.prm.x_rows) * p.xg_ld, &p.allocs);
+                    BD_CUDA(cudaMemset(p.xg, 0, size_t(md.prm.x_rows) * p.xg_ld * 2));
+                }
+                const std::vector<CUtensorMap> xmaps = mtd_x_maps(md.prm, p.xg, p.xg_ld);
+                CUtensorMap* dp = dmalloc<CUtensorMap>(pmaps.size(), &p.allocs);
+                CUtensorMap* dx = dmalloc<CUtensorMap>(xmaps.size(), &p.allocs);
+                BD_CUDA(cudaMemcpy(dp, pmaps.data(), pmaps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+                BD_CUDA(cudaMemcpy(dx, xmaps.data(), xmaps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+                md.prm.plane_maps = dp;
+                md.prm.x_maps = dx;
+                md.prm.out = D;
+                md.ok = true;
+                p.mtd[l][gi] = md;
+            }
+            if (!ok)
+                for (uint64_t l = 0; l < nL; ++l) p.mtd[l][gi].ok = false;
+        }
+    }
+
     // K23 (mt4.cu): base GEMM + every tenant plane as FP4 MMAs in one persistent
     // kernel. Slots are ordered by tenant id and, within a tenant, by request id,
     // so the schedule (and every output bit) is independent of the batch order.
@@ -1093,6 +1170,7 @@ struct PoolImpl {
         // K23 fuses the bf16 base GEMM: not for an int8 backbone
         if (!i8 && (delta_mode == "mt4" || (delta_mode == "auto" && mean_per_tenant >= k23_min_requests(B))))
             plan_mt4_groups(*p, by_t);
+        if (delta_mode == "mtd") plan_mtd_groups(*p, by_t);
         if (delta_mode == "lut" || delta_mode == "auto") plan_lut_groups(*p);
         // groups already served by K23 keep no LUT plan
         for (uint64_t l = 0; l < p->mt4.size(); ++l)
@@ -1147,6 +1225,7 @@ struct PoolImpl {
 
     bool lut_ok(const Plan& p, uint64_t l, int gi) const { return p.lut.size() > l && p.lut[l][gi].ok; }
     bool mt4_ok(const Plan& p, uint64_t l, int gi) const { return p.mt4.size() > l && p.mt4[l][gi].ok; }
+    bool mtd_ok(const Plan& p, uint64_t l, int gi) const { return p.mtd.size() > l && p.mtd[l][gi].ok; }
     ProjOut group_out(const Plan& p, uint64_t l, int gi, const GemmPlan& g) const {
         if (mt4_ok(p, l, gi)) {
             const Mt4Params& f = p.mt4[l][gi].prm;
@@ -1156,6 +1235,11 @@ struct PoolImpl {
             o.pstride = size_t(p.B) * f.M;
             o.D = nullptr;
             o.M = f.M;
+            return o;
+        }
+        if (mtd_ok(p, l, gi)) {  // one delta partial per K split
+            ProjOut o = proj_out(g, true);
+            o.dsplits = p.mtd[l][gi].prm.ksplit;
             return o;
         }
         if (lut_ok(p, l, gi)) {
@@ -1187,6 +1271,14 @@ struct PoolImpl {
         if (mt4_ok(p, l, group)) {
             prof(BD_PROF_XQ_PREP, s, [&] { xp_prep_launch(X, ldx, cols, B, p.xpk, s); });
             prof(BD_PROF_FUSED_QKV + group, s, [&] { mt4_launch(p.mt4[l][group].prm, s); });
+            return;
+        }
+        if (mtd_ok(p, l, group)) {
+            // K2 and K3d both hold the SM's tensor memory: one after the other
+            const Plan::Md& md = p.mtd[l][group];
+            prof(BD_PROF_XQ_PREP, s, [&] { mtd_gather_launch(X, ldx, cols, md.gat, md.prm.n_ten, p.xg, p.xg_ld, s); });
+            prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm(g, l, group, mw, mx, s); });
+            prof(BD_PROF_DELTA_QKV + group, s, [&] { mtd_launch(md.prm, s); });
             return;
         }
         if (lut_ok(p, l, group)) {
@@ -1329,6 +1421,7 @@ struct PoolImpl {
             char c = 'U';
             if (a.n_layers == 0) c = '-';
             else if (mt4_ok(p, 0, gi)) c = 'T';
+            else if (mtd_ok(p, 0, gi)) c = 'D';
             else if (lut_ok(p, 0, gi)) c = 'L';
             stats.delta_paths[gi] = c;
         }

@@ -170,3 +170,15 @@ def test_int8_backbone_m7_gqa_B64_T16(cuda, port):
     """int8 backbone at batch 64 (256 MMA columns of pieces), GQA, 4 requests per tenant: the
     LUT (K23 fuses a bf16 GEMM and is not planned for an int8 backbone)."""
     assert run_config(port, dict(M7, n_layers=1), 16, 64, steps=1, expect_paths="LLLL", int8=True) <= 1e-2
+
+
+@pytest.mark.parametrize("arch,n_layers,tenants,batch", [
+    (M7, 1, 1, 64),     # configs[3] T=1: one tenant, 64 requests (N = 64)
+    (M7, 1, 4, 64),     # configs[3] T=4: 16 requests per tenant
+    (L7, 2, 3, 40),     # 14/13/13 requests: N padded to 16, 2 layers
+])
+def test_k3d_many_requests_per_tenant(cuda, port, monkeypatch, arch, n_layers, tenants, batch):
+    """K3d (mtd.cu): a tenant's plane expanded once to bf16 +-1 in TMEM and applied to all
+    of its requests as the N of a kind::f16 MMA, against the oracle."""
+    monkeypatch.setenv("BD_DELTA", "mtd")
+    assert run_config(port, dict(arch, n_layers=n_layers), tenants, batch, steps=2, expect_paths="DDDD") <= 1e-2
