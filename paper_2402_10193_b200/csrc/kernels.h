@@ -154,6 +154,9 @@ void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stre
 // ---- K3d: tenants with many requests, dense tensor-core delta (mtd.cu) ----
 constexpr int kMtdMaxTenants = 8;
 constexpr int kMtdMaxN = 64;  // requests per tenant (MMA N, padded to 16)
+// mean requests per tenant from which the auto policy takes K3d (measured on M7 B=64: T=4
+// 16 requests/tenant 5 766 vs K23 5 072 tok/s, T=1 7 795 vs 5 089)
+constexpr double kMtdMinRequests = 8.0;
 struct MtdTenant {
     std::vector<int> reqs;  // batch indices
     int n_planes[kLutMaxSegs];

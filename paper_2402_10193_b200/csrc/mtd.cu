@@ -35,7 +35,7 @@ void note_launch();
 
 namespace {
 
-constexpr int kThreads = 32 * 6;  // producer, 4 expanders, issuer
+constexpr int kThreads = 32 * 7;  // producer, 4 expanders, issuer, second producer
 constexpr int kRing = 4;
 constexpr uint32_t kPlaneBytes = 128 * 32;                          // [128 rows x 32 B]
 constexpr uint32_t kXBytesMax = 4 * kMtdMaxN * 128;                  // 4 x [N rows x 128 B]
@@ -106,27 +106,32 @@ __global__ void __launch_bounds__(kThreads, 1) mtd_kernel(const __grid_constant_
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
 
-    if (warp == 0) {
-        // ---- TMA producer ----
+    if (warp == 0 || warp == 6) {
+        // ---- TMA producers: two warps take alternate stages (ring slots {p, p + 2} belong to
+        // producer p, so no slot is ever armed out of order); copies issued by one thread
+        // complete about one at a time ----
+        const int prod = warp == 0 ? 0 : 1;
         const uint64_t pol_stream = policy_evict_first();
         const uint64_t pol_keep = policy_evict_last();
         griddep_wait();  // PDL: X (gathered by the previous kernel)
-        int s = 0;
+        int s = 0, gidx = 0;
         uint32_t ph = 0;
         for (int t = t0; t < t1; ++t) {
             const Task k = task_of(p, t);
             const CUtensorMap* pmap = p.plane_maps + k.ten * kLutMaxSegs + k.seg;
             const CUtensorMap* xmap = p.x_maps + k.ten;
             const uint32_t xbytes = uint32_t(p.n_pad[k.ten]) * 128;
-            for (int c = k.c0; c < k.c1; ++c) {
-                mbar_wait_w(&empty[s], ph ^ 1);
-                uint8_t* sp = smem + s * kStageBytes;
-                mbar_arrive_expect_tx_w(&full[s], kPlaneBytes + 4 * xbytes);
-                tma_load_2d_w(sp, pmap, &full[s], c * 32, k.row, pol_stream);
+            for (int c = k.c0; c < k.c1; ++c, ++gidx) {
+                if ((gidx & 1) == prod) {
+                    mbar_wait_w(&empty[s], ph ^ 1);
+                    uint8_t* sp = smem + s * kStageBytes;
+                    mbar_arrive_expect_tx_w(&full[s], kPlaneBytes + 4 * xbytes);
+                    tma_load_2d_w(sp, pmap, &full[s], c * 32, k.row, pol_stream);
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    tma_load_2d_w(sp + kPlaneBytes + q * xbytes, xmap, &full[s], c * 256 + q * 64, p.x_row0[k.ten],
-                                  pol_keep);
+                    for (int q = 0; q < 4; ++q)
+                        tma_load_2d_w(sp + kPlaneBytes + q * xbytes, xmap, &full[s], c * 256 + q * 64,
+                                      p.x_row0[k.ten], pol_keep);
+                }
                 if (++s == kRing) {
                     s = 0;
                     ph ^= 1;
@@ -134,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, 1) mtd_kernel(const __grid_constant_
             }
         }
     } else if (warp == 5) {
-        // ---- MMA issuer ----
+        // ---- MMA issuer (whole warp, one elected lane issues) ----
         int s = 0, e = 0, d = 0;
         uint32_t ph = 0, eph = 0;
         for (int t = t0; t < t1; ++t) {

@@ -1161,18 +1161,27 @@ struct PoolImpl {
             p->xq_dim = tmap_pieces(xq, B, a.dim, ld8_dim, p->g_qkv.bn);
             p->xq_inter = tmap_pieces(xq, B, a.intermediate, ld8_inter, p->g_qkv.bn);
         }
-        // K3 variant for the whole batch (one backend, chosen by requests per tenant): K23
-        // when tenants average k23_min_requests(B) requests or more (each plane is then read
-        // once per slot of up to 4 requests), the byte LUT beside K2 otherwise (one job per
-        // request); the mean, not the maximum, so one busy tenant does not move a batch of
-        // single-request tenants onto K23 (measured slower there)
+        // K3 variant for the whole batch (one backend, chosen by requests per tenant): K3d when
+        // tenants average kMtdMinRequests or more (a plane expanded once serves all of its
+        // tenant's requests as MMA columns), else K23 from k23_min_requests(B) (each plane read
+        // once per slot of up to 4 requests), else the byte LUT beside K2 (one job per request);
+        // the mean, not the maximum, so one busy tenant does not move a batch of single-request
+        // tenants off the LUT (measured slower there). Groups a variant cannot
+        // plan fall through to the next one.
         const double mean_per_tenant = order.empty() ? 0.0 : double(B) / double(order.size());
+        if (delta_mode == "mtd" || (delta_mode == "auto" && mean_per_tenant >= kMtdMinRequests))
+            plan_mtd_groups(*p, by_t);
         // K23 fuses the bf16 base GEMM: not for an int8 backbone
         if (!i8 && (delta_mode == "mt4" || (delta_mode == "auto" && mean_per_tenant >= k23_min_requests(B))))
             plan_mt4_groups(*p, by_t);
-        if (delta_mode == "mtd") plan_mtd_groups(*p, by_t);
         if (delta_mode == "lut" || delta_mode == "auto") plan_lut_groups(*p);
-        // groups already served by K23 keep no LUT plan
+        // groups already served by K3d keep no K23 / LUT plan, groups served by K23 no LUT plan
+        for (uint64_t l = 0; l < p->mtd.size(); ++l)
+            for (int gi = 0; gi < 4; ++gi)
+                if (p->mtd[l][gi].ok) {
+                    if (p->mt4.size() > l) p->mt4[l][gi].ok = false;
+                    if (p->lut.size() > l) p->lut[l][gi] = Plan::Lut{};
+                }
         for (uint64_t l = 0; l < p->mt4.size(); ++l)
             for (int gi = 0; gi < 4; ++gi)
                 if (p->mt4[l][gi].ok && !p->lut.empty()) p->lut[l][gi] = Plan::Lut{};

@@ -138,11 +138,18 @@ def test_config2_l7_stack_B16(cuda, port, tenants):
                       expect_paths="LLLL") <= 1e-2
 
 
-@pytest.mark.parametrize("tenants,paths", [(1, "TTTT"), (16, "TTTT"), (64, "LLLL")])
+@pytest.mark.parametrize("tenants,paths", [(1, "DDDD"), (4, "DDDD"), (16, "TTTT"), (64, "LLLL")])
 def test_config3_m7_gqa_B64(cuda, port, tenants, paths):
-    """configs[3]: Mistral-7B GQA (kv_dim 1024 < dim), batch 64, tenant sweep ends + middle."""
+    """configs[3]: Mistral-7B GQA (kv_dim 1024 < dim), batch 64, tenant sweep through the
+    default dispatch (K3d from 8 requests per tenant, K23 from 2, the byte LUT below)."""
     assert run_config(port, dict(M7, n_layers=1), tenants, 64, steps=2, seed=100 + tenants,
                       expect_paths=paths) <= 1e-2
+
+
+def test_config3_k23_one_tenant_B64(cuda, port, monkeypatch):
+    """K23 (slots of 4 requests) kept under test at one tenant x 64 requests (forced)."""
+    monkeypatch.setenv("BD_DELTA", "mt4")
+    assert run_config(port, dict(M7, n_layers=1), 1, 64, steps=2, seed=101, expect_paths="TTTT") <= 1e-2
 
 
 def test_config4_l70_layer_T32_B32(cuda, port):
