@@ -154,9 +154,12 @@ void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stre
 // ---- K3d: tenants with many requests, dense tensor-core delta (mtd.cu) ----
 constexpr int kMtdMaxTenants = 8;
 constexpr int kMtdMaxN = 64;  // requests per tenant (MMA N, padded to 16)
-// mean requests per tenant from which the auto policy takes K3d (measured on M7 B=64: T=4
-// 16 requests/tenant 5 766 vs K23 5 072 tok/s, T=1 7 795 vs 5 089)
-constexpr double kMtdMinRequests = 8.0;
+// the auto policy takes K3d from 16 requests per tenant at batch >= 64. Measured (tok/s):
+// M7 B=64 T=1 7 963 vs K23 5 089, T=4 (16/tenant) 6 272 vs 5 072, T=8 (8/tenant) 4 641 vs
+// K23 5 126; L7 B=16 T=1 (16/tenant) 2 807 vs the byte LUT 3 129 (its 16 jobs read one plane,
+// mostly from L2, and it runs beside K2 while K3d runs after it)
+constexpr double kMtdMinRequests = 16.0;
+constexpr int kMtdMinBatch = 64;
 struct MtdTenant {
     std::vector<int> reqs;  // batch indices
     int n_planes[kLutMaxSegs];

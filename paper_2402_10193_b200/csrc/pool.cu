@@ -1162,14 +1162,15 @@ struct PoolImpl {
             p->xq_inter = tmap_pieces(xq, B, a.intermediate, ld8_inter, p->g_qkv.bn);
         }
         // K3 variant for the whole batch (one backend, chosen by requests per tenant): K3d when
-        // tenants average kMtdMinRequests or more (a plane expanded once serves all of its
+        // tenants average kMtdMinRequests or more at batch >= kMtdMinBatch (a plane expanded once serves all of its
         // tenant's requests as MMA columns), else K23 from k23_min_requests(B) (each plane read
         // once per slot of up to 4 requests), else the byte LUT beside K2 (one job per request);
         // the mean, not the maximum, so one busy tenant does not move a batch of single-request
         // tenants off the LUT (measured slower there). Groups a variant cannot
         // plan fall through to the next one.
         const double mean_per_tenant = order.empty() ? 0.0 : double(B) / double(order.size());
-        if (delta_mode == "mtd" || (delta_mode == "auto" && mean_per_tenant >= kMtdMinRequests))
+        if (delta_mode == "mtd" ||
+            (delta_mode == "auto" && mean_per_tenant >= kMtdMinRequests && B >= kMtdMinBatch))
             plan_mtd_groups(*p, by_t);
         // K23 fuses the bf16 base GEMM: not for an int8 backbone
         if (!i8 && (delta_mode == "mt4" || (delta_mode == "auto" && mean_per_tenant >= k23_min_requests(B))))
