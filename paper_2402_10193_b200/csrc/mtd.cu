@@ -22,7 +22,8 @@
 //     D[split][r][m] for the tenant's real requests; K is split so the grid fills the GPU
 //     (a single tenant has few row tiles), the consumer sums the split partials in order.
 // Exact like K2: +-1 and bf16 x are exact in the MMA, f32 accumulation.
-// One CTA per SM (512 TMEM columns): runs after K2, not beside it.
+// One CTA per SM (512 TMEM columns): runs after K2, not beside it (a 256-column variant with
+// 128-column chunks beside K2 on the side stream measured slower: DESIGN.md §7.0).
 #include <algorithm>
 #include <vector>
 
@@ -258,7 +259,8 @@ __global__ void __launch_bounds__(kThreads, 1) mtd_kernel(const __grid_constant_
 }
 
 // Xp[row0_t + i] = X[req_t[i]] (i < n_t; zero rows up to n_pad_t), each 32-column block in
-// the MMA's column order (2 i <- i, 2 i + 1 <- i + 16); grid (gathered rows, column chunks)
+// the MMA's column order (2 i <- i, 2 i + 1 <- i + 16); grid (gathered rows, column chunks),
+// thread = one 32-column block (4 x 16-byte loads, the pairs interleaved with PRMT)
 __global__ void mtd_gather_kernel(const uint16_t* __restrict__ X, int ldx, int K, const MtdGather g,
                                   uint16_t* __restrict__ Xp, int ldp) {
     griddep_wait();
@@ -267,11 +269,27 @@ __global__ void mtd_gather_kernel(const uint16_t* __restrict__ X, int ldx, int K
     while (t + 1 < kMtdMaxTenants && row >= g.row0[t] + g.n_pad[t]) ++t;
     const int i = row - g.row0[t];
     const int r = i < g.n_req[t] ? g.req[t][i] : -1;
-    uint16_t* dst = Xp + static_cast<size_t>(row) * ldp;
-    for (int k = blockIdx.y * blockDim.x + threadIdx.x; k < K; k += gridDim.y * blockDim.x) {
-        const int blk = k & ~31, e = k & 31;
-        const int src = blk + ((e & 1) ? 16 + (e >> 1) : (e >> 1));
-        dst[k] = r >= 0 ? X[static_cast<size_t>(r) * ldx + src] : uint16_t(0);
+    uint4* dst = reinterpret_cast<uint4*>(Xp + static_cast<size_t>(row) * ldp);
+    const uint4* src = r >= 0 ? reinterpret_cast<const uint4*>(X + static_cast<size_t>(r) * ldx) : nullptr;
+    for (int b = blockIdx.y * blockDim.x + threadIdx.x; b * 32 < K; b += gridDim.y * blockDim.x) {
+        uint4 lo0 = make_uint4(0, 0, 0, 0), lo1 = lo0, hi0 = lo0, hi1 = lo0;  // columns 0-7, 8-15, 16-23, 24-31
+        if (src) {
+            lo0 = src[4 * b];
+            lo1 = src[4 * b + 1];
+            hi0 = src[4 * b + 2];
+            hi1 = src[4 * b + 3];
+        }
+        // output word m = (column m, column m + 16), m < 16
+        const uint32_t l[8] = {lo0.x, lo0.y, lo0.z, lo0.w, lo1.x, lo1.y, lo1.z, lo1.w};
+        const uint32_t h[8] = {hi0.x, hi0.y, hi0.z, hi0.w, hi1.x, hi1.y, hi1.z, hi1.w};
+        uint32_t o[16];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            o[2 * q] = __byte_perm(l[q], h[q], 0x5410);      // (column 2q, column 2q + 16)
+            o[2 * q + 1] = __byte_perm(l[q], h[q], 0x7632);  // (column 2q + 1, column 2q + 17)
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) dst[4 * b + v] = make_uint4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
     }
 }
 
@@ -339,7 +357,8 @@ std::vector<CUtensorMap> mtd_x_maps(const MtdParams& p, const void* Xp, int ldp)
 void mtd_gather_launch(const void* X, int ldx, int K, const MtdGather& g, int n_ten, void* Xp, int ldp,
                        cudaStream_t stream) {
     (void)n_ten;
-    BD_CUDA(launch_pdl(mtd_gather_kernel, dim3(g.rows, (K + 2047) / 2048), dim3(256), 0, stream,
+    require(K % 32 == 0 && ldx % 8 == 0 && ldp % 8 == 0, BD_ERR_BAD_ARGUMENT, "K3d gather: alignment");
+    BD_CUDA(launch_pdl(mtd_gather_kernel, dim3(g.rows, (K / 32 + 31) / 32), dim3(32), 0, stream,
                        static_cast<const uint16_t*>(X), ldx, K, g, static_cast<uint16_t*>(Xp), ldp));
     note_launch();
     BD_CUDA(cudaGetLastError());
