@@ -74,6 +74,13 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// 16-byte shared-memory load by shared-window address (keeps LDS, not a generic LD)
+__device__ __forceinline__ void lds128(uint32_t addr, uint32_t* v) {
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                 : "r"(addr));
+}
+
 // warp-wide wait: one lane polls (try_wait ~60 cycles on a completed phase; a
 // 32-lane vote loop measured ~150), then the warp reconverges
 __device__ __forceinline__ void mbar_wait_w(uint64_t* bar, uint32_t parity) {

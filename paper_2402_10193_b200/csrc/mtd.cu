@@ -13,9 +13,14 @@
 //   * a task = (tenant, 128-row tile); its stages are 256-column chunks: a [128 rows x 32 B]
 //     plane box (TMA, reference layout) and the tenant's X rows for the chunk (TMA, 4 boxes
 //     of [N_t rows x 64 columns], 128-byte swizzle: K2's B-operand layout);
-//   * 4 expander warps (thread = tile row = TMEM lane) turn a chunk's 8 plane words into 256
-//     bf16 +-1.0 (two per 32-bit TMEM column, one shift + one LOP3: see expand_bf16x2) in one
-//     of two 128-column TMEM entries;
+//   * 8 expander warps (two per TMEM lane quadrant, thread = tile row = TMEM lane, each warp
+//     half of the chunk) turn a chunk's 8 plane words into 256 bf16 +-1.0 (two per 32-bit
+//     TMEM column, one shift + one LOP3: see expand_bf16x2) in one of three 128-column TMEM
+//     entries; a ring of 6 stages (two producer warps) keeps the loads ahead.
+//     Measured (ncu, M7 gate/up, 4 tenants): a skeleton with no loads, expansion or MMAs
+//     takes ~45 % of the kernel (mbarrier / tcgen05.commit round trips per chunk), the
+//     expansion ~45 %, loads and MMAs the rest: 4 -> 8 expanders, 2 -> 3 entries and
+//     4 -> 6 stages took gate/up 77 -> 70 us at 4 tenants, 35 -> 29 us at 1;
 //   * an issuer warp runs 16 MMAs (M = 128, N = N_t, K = 16, A from TMEM, B from smem) per
 //     chunk into one of two f32 accumulators (N_t columns), accumulating over the task's K;
 //   * the epilogue (the expander warps, deferred by one chunk) applies alpha and writes
@@ -36,15 +41,22 @@ void note_launch();
 
 namespace {
 
-constexpr int kThreads = 32 * 7;  // producer, 4 expanders, issuer, second producer
-constexpr int kRing = 4;
+constexpr int kExpanders = 8;                     // expander warps 1..8 (4 measured slower)
+constexpr int kHalves = kExpanders / 4;           // expander warps per TMEM lane quadrant
+constexpr int kIssuer = kExpanders + 1;           // MMA issuer warp
+constexpr int kProducer2 = kExpanders + 2;        // second TMA producer warp
+constexpr int kThreads = 32 * (kExpanders + 3);
+constexpr int kRing = 6;  // 4 measured slower at 4 tenants
 constexpr uint32_t kPlaneBytes = 128 * 32;                          // [128 rows x 32 B]
 constexpr uint32_t kXBytesMax = 4 * kMtdMaxN * 128;                  // 4 x [N rows x 128 B]
 constexpr uint32_t kStageBytes = ((kPlaneBytes + kXBytesMax) + 1023) / 1024 * 1024;
 constexpr uint32_t kSmem = 1024 + kRing * kStageBytes + 256;
-// TMEM (512 columns): two A entries of 128 columns (K = 256 bf16), two accumulators of
+
+// TMEM (512 columns): kEntries A entries of 128 columns (K = 256 bf16), two accumulators of
 // kMtdMaxN columns
-constexpr uint32_t kColA = 0, kEntryCols = 128, kColAcc = 256;
+constexpr int kEntries = 3;
+constexpr uint32_t kColA = 0, kEntryCols = 128, kColAcc = kEntries * kEntryCols;
+static_assert(kColAcc + 2 * kMtdMaxN <= 512, "TMEM budget");
 
 struct Task {
     int ten, seg, m0, row, c0, c1;  // chunks [c0, c1) of the K split
@@ -79,9 +91,9 @@ __global__ void __launch_bounds__(kThreads, 1) mtd_kernel(const __grid_constant_
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRing * kStageBytes);
     uint64_t* empty = full + kRing;
-    uint64_t* a_full = empty + kRing;  // [2]
-    uint64_t* a_free = a_full + 2;     // [2]
-    uint64_t* acc_full = a_free + 2;   // [2]
+    uint64_t* a_full = empty + kRing;         // [kEntries]
+    uint64_t* a_free = a_full + kEntries;     // [kEntries]
+    uint64_t* acc_full = a_free + kEntries;   // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 2);
     const uint32_t warp = warp_id(), lane = lane_id();
     const int t0 = static_cast<int>(static_cast<long long>(p.n_tasks) * blockIdx.x / gridDim.x);
@@ -92,11 +104,11 @@ __global__ void __launch_bounds__(kThreads, 1) mtd_kernel(const __grid_constant_
                 mbar_init(&full[s], 1);
                 mbar_init(&empty[s], 1);
             }
-            for (int i = 0; i < 2; ++i) {
-                mbar_init(&a_full[i], 4);
+            for (int i = 0; i < kEntries; ++i) {
+                mbar_init(&a_full[i], kExpanders);
                 mbar_init(&a_free[i], 1);
-                mbar_init(&acc_full[i], 1);
             }
+            for (int i = 0; i < 2; ++i) mbar_init(&acc_full[i], 1);
             fence_mbar_init();
         }
         __syncwarp();
@@ -107,7 +119,7 @@ __global__ void __launch_bounds__(kThreads, 1) mtd_kernel(const __grid_constant_
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
 
-    if (warp == 0 || warp == 6) {
+    if (warp == 0 || warp == kProducer2) {
         // ---- TMA producers: two warps take alternate stages (ring slots {p, p + 2} belong to
         // producer p, so no slot is ever armed out of order); copies issued by one thread
         // complete about one at a time ----
@@ -139,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1) mtd_kernel(const __grid_constant_
                 }
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == kIssuer) {
         // ---- MMA issuer (whole warp, one elected lane issues) ----
         int s = 0, e = 0, d = 0;
         uint32_t ph = 0, eph = 0;
@@ -165,8 +177,10 @@ __global__ void __launch_bounds__(kThreads, 1) mtd_kernel(const __grid_constant_
                 tc_commit_w(&a_free[e]);
                 tc_commit_w(&empty[s]);
                 if (c == k.c1 - 1) tc_commit_w(&acc_full[d]);
-                e ^= 1;
-                if (e == 0) eph ^= 1;
+                if (++e == kEntries) {
+                    e = 0;
+                    eph ^= 1;
+                }
                 if (++s == kRing) {
                     s = 0;
                     ph ^= 1;
@@ -176,7 +190,8 @@ __global__ void __launch_bounds__(kThreads, 1) mtd_kernel(const __grid_constant_
         }
     } else {
         // ---- expanders: thread = tile row = TMEM lane ----
-        const uint32_t q4 = warp & 3;
+        const uint32_t q4 = warp & 3;  // a warp reaches TMEM lanes 32 (warp % 4) ..
+        const uint32_t half = (warp - 1) / 4;  // which part of the chunk (and of the epilogue)
         const uint32_t trow = q4 * 32 + lane;
         const uint32_t lane_base = (q4 * 32) << 16;
         griddep_wait();  // D is still read by the previous kernel's consumer
@@ -190,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1) mtd_kernel(const __grid_constant_
             tc_fence_after();
             const int n = p.n_req[pend_ten];
             const float alpha = p.alpha[pend_ten][pend_seg];
-            for (int c0 = 0; c0 < n; c0 += 16) {
+            for (int c0 = 16 * int(half); c0 < n; c0 += 16 * kHalves) {
                 uint32_t v[16];
                 tmem_ld16(tbase + lane_base + kColAcc + pend_d * kMtdMaxN + c0, v);
                 tmem_ld_wait();
@@ -207,15 +222,17 @@ __global__ void __launch_bounds__(kThreads, 1) mtd_kernel(const __grid_constant_
         for (int t = t0; t < t1; ++t) {
             const Task k = task_of(p, t);
             for (int c = k.c0; c < k.c1; ++c) {
-                mbar_wait(&full[s], ph);
-                if (n_entries >= 2) mbar_wait(&a_free[e], eph ^ 1);  // the entry's previous MMAs done
+                mbar_wait(&full[s], ph);  // every lane polls (one polling lane measured slower)
+                if (n_entries >= kEntries) mbar_wait(&a_free[e], eph ^ 1);  // the entry's previous MMAs done
                 tc_fence_after();
-                const uint4* rowp = reinterpret_cast<const uint4*>(smem + s * kStageBytes + trow * 32);
-                const uint4 v0 = rowp[0], v1 = rowp[1];
-                const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-                const uint32_t ent = tbase + lane_base + kColA + e * kEntryCols;
+                constexpr int kWords = 8 / kHalves;  // plane words of this warp's part of the row
+                uint32_t w[kWords];
+                const uint32_t rowp = smem_u32(smem + s * kStageBytes + trow * 32 + half * 4 * kWords);
 #pragma unroll
-                for (int h = 0; h < 4; ++h) {  // 64 columns (2 words) -> 32 TMEM columns
+                for (int v = 0; v < kWords / 4; ++v) lds128(rowp + 16 * v, w + 4 * v);
+                const uint32_t ent = tbase + lane_base + kColA + e * kEntryCols + half * 16 * kWords;
+#pragma unroll
+                for (int h = 0; h < kWords / 2; ++h) {  // 64 columns (2 words) -> 32 TMEM columns
                     uint32_t a[32];
 #pragma unroll
                     for (int u = 0; u < 2; ++u) {
@@ -236,8 +253,10 @@ __global__ void __launch_bounds__(kThreads, 1) mtd_kernel(const __grid_constant_
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&a_full[e]);
                 ++n_entries;
-                e ^= 1;
-                if (e == 0) eph ^= 1;
+                if (++e == kEntries) {
+                    e = 0;
+                    eph ^= 1;
+                }
                 if (++s == kRing) {
                     s = 0;
                     ph ^= 1;
