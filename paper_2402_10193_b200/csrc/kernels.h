@@ -174,6 +174,7 @@ struct MtdGather {
 struct MtdParams {
     int n_tasks, tiles, M, K, n_segs, n_ten, x_rows, grid;
     int n_chunks, ksplit, chunks_per_split;  // 256-column chunks; K splits (delta partials)
+    int ring, stage_bytes;                   // stage ring sized for the launch's largest N_t
     size_t dstride;                          // elements between delta partials (batch x M)
     int seg_row0[kLutMaxSegs + 1];
     const CUtensorMap* plane_maps;  // device [tenant][seg]: box [128 rows x 32 B]

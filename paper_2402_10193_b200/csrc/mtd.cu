@@ -46,11 +46,13 @@ constexpr int kHalves = kExpanders / 4;           // expander warps per TMEM lan
 constexpr int kIssuer = kExpanders + 1;           // MMA issuer warp
 constexpr int kProducer2 = kExpanders + 2;        // second TMA producer warp
 constexpr int kThreads = 32 * (kExpanders + 3);
-constexpr int kRing = 6;  // 4 measured slower at 4 tenants
+// stage ring: as many stages as fit (6 at N_t = 64, up to kMaxRing at N_t = 16); the
+// ring depth hides the per-chunk barrier round trips (4 stages measured slower)
+constexpr int kMaxRing = 24;
 constexpr uint32_t kPlaneBytes = 128 * 32;                          // [128 rows x 32 B]
 constexpr uint32_t kXBytesMax = 4 * kMtdMaxN * 128;                  // 4 x [N rows x 128 B]
-constexpr uint32_t kStageBytes = ((kPlaneBytes + kXBytesMax) + 1023) / 1024 * 1024;
-constexpr uint32_t kSmem = 1024 + kRing * kStageBytes + 256;
+constexpr uint32_t kRingBytes = 6 * ((kPlaneBytes + kXBytesMax + 1023) / 1024 * 1024);
+constexpr uint32_t kSmem = 1024 + kRingBytes + 512;
 
 // TMEM (512 columns): kEntries A entries of 128 columns (K = 256 bf16), two accumulators of
 // kMtdMaxN columns
@@ -89,9 +91,11 @@ __device__ __forceinline__ uint32_t expand_bf16x2(uint32_t w) {
 __global__ void __launch_bounds__(kThreads, 1) mtd_kernel(const __grid_constant__ MtdParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRing * kStageBytes);
-    uint64_t* empty = full + kRing;
-    uint64_t* a_full = empty + kRing;         // [kEntries]
+    const int kRing = p.ring;
+    const uint32_t kStageBytes = uint32_t(p.stage_bytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRingBytes);
+    uint64_t* empty = full + kMaxRing;
+    uint64_t* a_full = empty + kMaxRing;      // [kEntries]
     uint64_t* a_free = a_full + kEntries;     // [kEntries]
     uint64_t* acc_full = a_free + kEntries;   // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 2);
@@ -362,6 +366,10 @@ bool plan_mtd(MtdParams& p, MtdGather& g, const std::vector<MtdTenant>& tens, co
     p.ksplit = (p.n_chunks + p.chunks_per_split - 1) / p.chunks_per_split;
     p.n_tasks = base_tasks * p.ksplit;
     p.grid = std::min(kNumSMs, p.n_tasks);
+    int max_pad = 16;
+    for (int t = 0; t < p.n_ten; ++t) max_pad = std::max(max_pad, p.n_pad[t]);
+    p.stage_bytes = int((kPlaneBytes + 4 * uint32_t(max_pad) * 128 + 1023) / 1024 * 1024);
+    p.ring = std::min(kMaxRing, int(kRingBytes / uint32_t(p.stage_bytes))) & ~1;  // even: two producers
     return true;
 }
 
