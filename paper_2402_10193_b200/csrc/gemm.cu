@@ -14,6 +14,11 @@
 //
 // Roofline: HBM — 2 bytes per weight element; at batch B the intensity is B
 // flop/byte, far below the tensor pipe's ridge point.
+//
+// Persistent: one CTA per resident slot walks its work units (row tile, K split) through
+// ONE continuous stage ring, with two TMEM accumulators so unit i + 1 accumulates while
+// four epilogue warps drain unit i: no per-unit pipeline refill or CTA launch. Measured
+// (ncu, M7 B=64 gate/up, 1120 units): 54 -> 43 us.
 #include <cstdlib>
 #include <cudaTypedefs.h>
 
@@ -31,7 +36,7 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // bf16 elements = 128 bytes = one swizzle row
 constexpr int kMaxStages = 8;
-constexpr int kGemmThreads = 128;
+constexpr int kGemmThreads = 256;  // producer, issuer, TMEM allocator, idle, 4 epilogue warps
 
 struct GemmSmemLayout {
     uint32_t a_bytes, b_bytes, stage_bytes, stages, total;
@@ -55,8 +60,8 @@ template <bool kI8>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     base_gemm_kernel(const __grid_constant__ CUtensorMap map_w,
                      const __grid_constant__ CUtensorMap map_x, float* __restrict__ partial,
-                     int M, int N_valid, int bn, int kb_total, int kb_per_split, int stages,
-                     const float* __restrict__ row_scale, const float* __restrict__ piece_scale) {
+                     int M, int N_valid, int bn, int kb_total, int kb_per_split, int splits, int n_units,
+                     int stages, const float* __restrict__ row_scale, const float* __restrict__ piece_scale) {
     extern __shared__ uint8_t smem_raw[];
     const unsigned long long t_entry = gtimer();
     unsigned long long t_wait = 0;
@@ -65,16 +70,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const GemmSmemLayout L = gemm_layout(bn, stages);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * L.stage_bytes);
     uint64_t* empty = full + kMaxStages;
-    uint64_t* done = empty + kMaxStages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    uint64_t* done = empty + kMaxStages;  // [2]: accumulator a complete
+    uint64_t* acc_free = done + 2;        // [2]: accumulator a drained by the epilogue
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 2);
 
     const uint32_t warp = warp_id(), lane = lane_id();
-    const int m0 = blockIdx.x * kBM;
-    const int split = blockIdx.y;
-    const int kb0 = split * kb_per_split;
-    const int kb1 = min(kb_total, kb0 + kb_per_split);
-    const int nkb = kb1 - kb0;
-    const uint32_t tmem_cols_needed = bn <= 32 ? 32 : (bn <= 64 ? 64 : (bn <= 128 ? 128 : 256));
+    const uint32_t acc_cols = bn <= 32 ? 32 : (bn <= 64 ? 64 : (bn <= 128 ? 128 : 256));
+    constexpr int kbk = kI8 ? 128 : kBK;  // K elements per 128-byte stage row
+    // work unit u = (row tile u / splits, K split u % splits); CTA b takes b, b + grid, ...
+    auto unit = [&](int u, int& m0, int& split, int& kb0, int& nkb) {
+        m0 = (u / splits) * kBM;
+        split = u % splits;
+        kb0 = split * kb_per_split;
+        nkb = min(kb_total, kb0 + kb_per_split) - kb0;
+    };
 
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&map_w);
@@ -83,15 +92,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(done, 1);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&done[a], 1);
+            mbar_init(&acc_free[a], 4);
+        }
         fence_mbar_init();
     }
     if (warp == 2) {
-        // allocation size must be a compile-time immediate
-        if (tmem_cols_needed == 32) tmem_alloc<32>(tmem_slot);
-        else if (tmem_cols_needed == 64) tmem_alloc<64>(tmem_slot);
-        else if (tmem_cols_needed == 128) tmem_alloc<128>(tmem_slot);
-        else tmem_alloc<256>(tmem_slot);
+        // two accumulators (unit i + 1 accumulates while unit i drains); the allocation
+        // size must be a compile-time immediate
+        if (acc_cols == 32) tmem_alloc<64>(tmem_slot);
+        else if (acc_cols == 64) tmem_alloc<128>(tmem_slot);
+        else if (acc_cols == 128) tmem_alloc<256>(tmem_slot);
+        else tmem_alloc<512>(tmem_slot);
     }
     tc_fence_before();
     __syncthreads();
@@ -99,96 +112,120 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t taddr = *tmem_slot;
 
     if (warp == 0 && lane == 0) {
-        // ---- TMA producer ----
+        // ---- TMA producer: one continuous ring over all of the CTA's units ----
         // The weights do not depend on the predecessor kernel: the first ring's worth is
         // requested before waiting for it (PDL), the activations only after.
         const uint64_t pol_w = policy_evict_first();  // weights stream once per step
+        int m0, split, kb0, nkb;
+        unit(blockIdx.x, m0, split, kb0, nkb);
         const int npre = min(nkb, stages);
         for (int i = 0; i < npre; ++i) {
             mbar_arrive_expect_tx(&full[i], L.stage_bytes);
-            tma_load_2d_hint(smem + i * L.stage_bytes, &map_w, &full[i], (kb0 + i) * (kI8 ? 128 : kBK), m0, pol_w);
+            tma_load_2d_hint(smem + i * L.stage_bytes, &map_w, &full[i], (kb0 + i) * kbk, m0, pol_w);
         }
         griddep_wait();  // PDL: the activations come from the previous kernel
         t_wait = gtimer();
-        for (int i = 0; i < nkb; ++i) {
-            const int s = i % stages;
-            const uint32_t round = i / stages;
-            uint8_t* a = smem + s * L.stage_bytes;
-            uint8_t* b = a + L.a_bytes;
-            const int kc = (kb0 + i) * (kI8 ? 128 : kBK);
-            if (i >= npre) {
-                mbar_wait(&empty[s], (round & 1) ^ 1);
-                mbar_arrive_expect_tx(&full[s], L.stage_bytes);
-                tma_load_2d_hint(a, &map_w, &full[s], kc, m0, pol_w);
+        int it = 0;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+            unit(u, m0, split, kb0, nkb);
+            for (int i = 0; i < nkb; ++i, ++it) {
+                const int s = it % stages;
+                const uint32_t round = it / stages;
+                uint8_t* a = smem + s * L.stage_bytes;
+                uint8_t* b = a + L.a_bytes;
+                const int kc = (kb0 + i) * kbk;
+                if (it >= npre) {
+                    mbar_wait(&empty[s], (round & 1) ^ 1);
+                    mbar_arrive_expect_tx(&full[s], L.stage_bytes);
+                    tma_load_2d_hint(a, &map_w, &full[s], kc, m0, pol_w);
+                }
+                tma_load_2d(b, &map_x, &full[s], kc, 0);
             }
-            tma_load_2d(b, &map_x, &full[s], kc, 0);
         }
     } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer ---- (consumes only what the producer's barriers release)
         const uint32_t idesc = kI8 ? idesc_s8s8_s32(kBM, bn) : idesc_bf16_f32(kBM, bn);
-        for (int i = 0; i < nkb; ++i) {
-            const int s = i % stages;
-            const uint32_t round = i / stages;
-            mbar_wait(&full[s], round & 1);
+        int it = 0, lu = 0;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++lu) {
+            int m0, split, kb0, nkb;
+            unit(u, m0, split, kb0, nkb);
+            const int acc = lu & 1;
+            if (lu >= 2) mbar_wait(&acc_free[acc], ((lu >> 1) - 1) & 1);
             tc_fence_after();
-            uint8_t* a = smem + s * L.stage_bytes;
-            uint8_t* b = a + L.a_bytes;
-            const uint64_t da = sdesc_k128(a), db = sdesc_k128(b);
+            const uint32_t tacc = taddr + acc * acc_cols;
+            for (int i = 0; i < nkb; ++i, ++it) {
+                const int s = it % stages;
+                const uint32_t round = it / stages;
+                mbar_wait(&full[s], round & 1);
+                tc_fence_after();
+                uint8_t* a = smem + s * L.stage_bytes;
+                uint8_t* b = a + L.a_bytes;
+                const uint64_t da = sdesc_k128(a), db = sdesc_k128(b);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {  // +32 bytes per K step (16 bf16 / 32 int8)
-                if (kI8) mma_i8_ss(taddr, da + 2 * k, db + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
-                else mma_bf16_ss(taddr, da + 2 * k, db + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
-            }
-            tc_commit(&empty[s]);
-        }
-        tc_commit(done);
-    }
-
-    // ---- epilogue: all 4 warps drain their 32 TMEM lanes ----
-    __syncwarp();
-    mbar_wait(done, 0);
-    tc_fence_after();
-    const int row = m0 + warp * 32 + lane;
-    float* out = partial + static_cast<size_t>(split) * N_valid * M;
-    for (int c0 = 0; c0 < bn; c0 += 16) {
-        uint32_t r[16];
-        tmem_ld16(taddr + ((warp * 32) << 16) + c0, r);
-        tmem_ld_wait();
-        if (nkb <= 0) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) r[j] = 0;
-        }
-        if (row < M) {
-            if (kI8) {
-                // 16 columns = 4 requests x kPieces (4) int32 accumulators
-                const float rs = row_scale[row];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int n = c0 / kPieces + q;
-                    if (n >= N_valid) break;
-                    double acc = 0.0;  // exact: |acc_p| < 2^31, piece scales are powers of two
-#pragma unroll
-                    for (int pc = 0; pc < kPieces; ++pc)
-                        acc += static_cast<double>(static_cast<int32_t>(r[q * kPieces + pc])) *
-                               static_cast<double>(piece_scale[n * kPieces + pc]);
-                    out[static_cast<size_t>(n) * M + row] = static_cast<float>(acc) * rs;
+                for (int k = 0; k < 4; ++k) {  // +32 bytes per K step (16 bf16 / 32 int8)
+                    if (kI8) mma_i8_ss(tacc, da + 2 * k, db + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
+                    else mma_bf16_ss(tacc, da + 2 * k, db + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
                 }
-            } else {
+                tc_commit(&empty[s]);
+            }
+            tc_commit(&done[acc]);
+        }
+    } else if (warp >= 4) {
+        // ---- epilogue: warps 4-7 drain their 32 TMEM lanes (lane quadrant = warp % 4) ----
+        const uint32_t q = warp & 3;
+        int lu = 0;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++lu) {
+            int m0, split, kb0, nkb;
+            unit(u, m0, split, kb0, nkb);
+            const int acc = lu & 1;
+            mbar_wait(&done[acc], (lu >> 1) & 1);
+            tc_fence_after();
+            const int row = m0 + q * 32 + lane;
+            float* out = partial + static_cast<size_t>(split) * N_valid * M;
+            for (int c0 = 0; c0 < bn; c0 += 16) {
+                uint32_t r[16];
+                tmem_ld16(taddr + ((q * 32) << 16) + acc * acc_cols + c0, r);
+                tmem_ld_wait();
+                if (nkb <= 0) {
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int n = c0 + j;
-                    if (n < N_valid) out[static_cast<size_t>(n) * M + row] = __uint_as_float(r[j]);
+                    for (int j = 0; j < 16; ++j) r[j] = 0;
+                }
+                if (row < M) {
+                    if (kI8) {
+                        // 16 columns = 4 requests x kPieces (4) int32 accumulators
+                        const float rs = row_scale[row];
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) {
+                            const int n = c0 / kPieces + g;
+                            if (n >= N_valid) break;
+                            double sum = 0.0;  // exact: |acc_p| < 2^31, piece scales are powers of two
+#pragma unroll
+                            for (int pc = 0; pc < kPieces; ++pc)
+                                sum += static_cast<double>(static_cast<int32_t>(r[g * kPieces + pc])) *
+                                       static_cast<double>(piece_scale[n * kPieces + pc]);
+                            out[static_cast<size_t>(n) * M + row] = static_cast<float>(sum) * rs;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const int n = c0 + j;
+                            if (n < N_valid) out[static_cast<size_t>(n) * M + row] = __uint_as_float(r[j]);
+                        }
+                    }
                 }
             }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_free[acc]);
         }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {
-        if (tmem_cols_needed == 32) tmem_dealloc<32>(taddr);
-        else if (tmem_cols_needed == 64) tmem_dealloc<64>(taddr);
-        else if (tmem_cols_needed == 128) tmem_dealloc<128>(taddr);
-        else tmem_dealloc<256>(taddr);
+        if (acc_cols == 32) tmem_dealloc<64>(taddr);
+        else if (acc_cols == 64) tmem_dealloc<128>(taddr);
+        else if (acc_cols == 128) tmem_dealloc<256>(taddr);
+        else tmem_dealloc<512>(taddr);
     }
     if (warp == 0 && lane == 0) trace_rec(TR_GEMM, t_entry, t_wait);
 }
@@ -288,6 +325,7 @@ GemmPlan plan_gemm(uint64_t M, uint64_t K, int batch, int smem_cap, bool i8) {
     p.kb_per_split = (kb + best_s - 1) / best_s;
     p.splits = (kb + p.kb_per_split - 1) / p.kb_per_split;
     p.m_tiles = m_tiles;
+    p.grid = slots;  // persistent: at most one CTA per slot, each walking its units
     return p;
 }
 
@@ -304,10 +342,10 @@ static void gemm_launch_t(const GemmPlan& p, const CUtensorMap& map_w, const CUt
                                      int(cudaSharedmemCarveoutMaxShared)));
         attr_set = true;
     }
-    dim3 grid(p.m_tiles, p.splits);
-    BD_CUDA(launch_pdl(base_gemm_kernel<kI8>, grid, dim3(kGemmThreads), size_t(p.smem), stream, map_w, map_x,
-                       partial, int(p.M), p.batch, p.bn, p.kb_total, p.kb_per_split, p.stages, row_scale,
-                       piece_scale));
+    const int n_units = p.m_tiles * p.splits;
+    BD_CUDA(launch_pdl(base_gemm_kernel<kI8>, dim3(std::min(n_units, p.grid)), dim3(kGemmThreads), size_t(p.smem),
+                       stream, map_w, map_x, partial, int(p.M), p.batch, p.bn, p.kb_total, p.kb_per_split, p.splits,
+                       n_units, p.stages, row_scale, piece_scale));
     note_launch();
     BD_CUDA(cudaGetLastError());
 }

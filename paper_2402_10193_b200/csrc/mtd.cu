@@ -286,6 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1) mtd_kernel(const __grid_constant_
 // thread = one 32-column block (4 x 16-byte loads, the pairs interleaved with PRMT)
 __global__ void mtd_gather_kernel(const uint16_t* __restrict__ X, int ldx, int K, const MtdGather g,
                                   uint16_t* __restrict__ Xp, int ldp) {
+    griddep_launch_dependents();  // K2's weight prefetch does not depend on the gathered X
     griddep_wait();
     const int row = blockIdx.x;
     int t = 0;
