@@ -1175,7 +1175,8 @@ struct PoolImpl {
         // K23 fuses the bf16 base GEMM: not for an int8 backbone
         if (!i8 && (delta_mode == "mt4" || (delta_mode == "auto" && mean_per_tenant >= k23_min_requests(B))))
             plan_mt4_groups(*p, by_t);
-        if (delta_mode == "lut" || delta_mode == "auto") plan_lut_groups(*p);
+        // forced K3d: groups it cannot plan (> kMtdMaxTenants tenants, ...) take the LUT
+        if (delta_mode == "lut" || delta_mode == "auto" || delta_mode == "mtd") plan_lut_groups(*p);
         // groups already served by K3d keep no K23 / LUT plan, groups served by K23 no LUT plan
         for (uint64_t l = 0; l < p->mtd.size(); ++l)
             for (int gi = 0; gi < 4; ++gi)
