@@ -230,8 +230,8 @@ int bd_pool_register_delta_file(bd_pool* pool, const char* id, const char* path,
 /* Host-only check of a .bdelta container (read_delta_file's validation, delta.cpp:265-334,
  * no device needed): *n_tensors = entries, *n_packed = packed entries, *max_planes = the
  * largest plane count. The pool serves packed projections with 1..4 planes per projection
- * and raw entries for norms / embed / lm_head; raw projection deltas (build_delta_file
- * with a policy that leaves a projection unquantised) and > 4 planes are rejected by
+ * and raw (f32) entries anywhere, projections included (a group with a raw projection delta
+ * takes the generic delta units + raw pass for that step); > 4 planes are rejected by
  * register_delta with BD_ERR_BAD_ARGUMENT (the reference's ServingPool would serve them). */
 int bd_bdelta_validate(const char* path, uint64_t* n_tensors, uint64_t* n_packed, uint64_t* max_planes);
 

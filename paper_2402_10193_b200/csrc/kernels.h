@@ -86,6 +86,18 @@ struct DeltaUnit {
 void delta_units_launch(const DeltaUnit* units_host, int n_units, const void* X, int ldx,
                         int cols, int batch, float* D, int out_rows, cudaStream_t stream);
 
+// ---- raw (unquantised f32) projection deltas, P:src/serve.cpp:27-35 (packed.cu) ----
+// D[req][row0 + r] += sum_k W[r][k] x_req[k] for the job's requests (after the units pass,
+// which zeroes D and leaves the rows of raw projections at 0)
+constexpr int kRawMaxReq = 16;
+struct RawJob {
+    const float* W;  // [rows x cols] f32, this rank's rows
+    int32_t row0, rows, n_req;
+    int32_t req[kRawMaxReq];
+};
+void raw_delta_launch(const RawJob* jobs, int n_jobs, const void* X, int ldx, int cols, float* D, int out_rows,
+                      cudaStream_t stream);
+
 // ---- K23: base GEMM + tenant deltas as FP4 (kind::mxf4) MMAs in one persistent kernel (mt4.cu) ----
 constexpr int kMt4MaxSlots = 64;
 constexpr int kMt4MaxReq = 4;   // requests per slot (MMA N = 8 pieces x n_req <= 32)

@@ -308,6 +308,71 @@ void packed_accumulate_launch(const uint8_t* bits, uint64_t rows, uint64_t cols,
     BD_CUDA(cudaGetLastError());
 }
 
+namespace {
+
+// raw projection deltas: block = 8 rows of one job (warp = row), f32 weights, bf16
+// activations, f32 sums (the reference sums in f32 too, serve.cpp:30-33), added to D
+constexpr int kRawJobsPerLaunch = 32;
+constexpr int kRawRowsPerBlock = 8;
+struct RawTable {
+    int n_jobs, cols, ldx, out_rows;
+    int block0[kRawJobsPerLaunch + 1];
+    RawJob j[kRawJobsPerLaunch];
+};
+
+__global__ void __launch_bounds__(32 * kRawRowsPerBlock)
+    raw_delta_kernel(const __grid_constant__ RawTable t, const uint16_t* __restrict__ X, float* __restrict__ D) {
+    int ji = 0;
+    while (ji + 1 < t.n_jobs && int(blockIdx.x) >= t.block0[ji + 1]) ++ji;
+    const RawJob& J = t.j[ji];
+    const int r = (int(blockIdx.x) - t.block0[ji]) * kRawRowsPerBlock + int(threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= J.rows) return;
+    const float* w = J.W + static_cast<size_t>(r) * t.cols;
+    for (int q0 = 0; q0 < J.n_req; q0 += 4) {
+        float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        for (int c = lane; c < t.cols; c += 32) {
+            const float wv = __ldg(w + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (q0 + i < J.n_req) acc[i] += wv * bf16_to_f32(X[static_cast<size_t>(J.req[q0 + i]) * t.ldx + c]);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            float v = acc[i];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0 && q0 + i < J.n_req) D[static_cast<size_t>(J.req[q0 + i]) * t.out_rows + J.row0 + r] += v;
+        }
+    }
+}
+
+}  // namespace
+
+void raw_delta_launch(const RawJob* jobs, int n_jobs, const void* X, int ldx, int cols, float* D, int out_rows,
+                      cudaStream_t stream) {
+    for (int first = 0; first < n_jobs; first += kRawJobsPerLaunch) {
+        RawTable tab{};
+        tab.n_jobs = std::min(kRawJobsPerLaunch, n_jobs - first);
+        tab.cols = cols;
+        tab.ldx = ldx;
+        tab.out_rows = out_rows;
+        int blocks = 0;
+        for (int i = 0; i < tab.n_jobs; ++i) {
+            tab.j[i] = jobs[first + i];
+            require(tab.j[i].W && tab.j[i].n_req >= 1 && tab.j[i].n_req <= kRawMaxReq, BD_ERR_BAD_ARGUMENT,
+                    "raw delta: bad job");
+            tab.block0[i] = blocks;
+            blocks += (tab.j[i].rows + kRawRowsPerBlock - 1) / kRawRowsPerBlock;
+        }
+        tab.block0[tab.n_jobs] = blocks;
+        if (blocks == 0) continue;
+        raw_delta_kernel<<<blocks, 32 * kRawRowsPerBlock, 0, stream>>>(tab, static_cast<const uint16_t*>(X), D);
+        note_launch();
+        BD_CUDA(cudaGetLastError());
+    }
+}
+
 void delta_units_launch(const DeltaUnit* units, int n_units, const void* X, int ldx, int cols,
                         int batch, float* D, int out_rows, cudaStream_t stream) {
     BD_CUDA(cudaMemsetAsync(D, 0, static_cast<size_t>(batch) * out_rows * sizeof(float), stream));

@@ -113,6 +113,8 @@ struct Tenant {
     bool resident = false, loaded = false;
     // [layer][proj] -> planes (this rank's row slice)
     std::vector<std::array<std::vector<Plane>, P_COUNT>> proj;
+    // [layer][proj] -> raw (unquantised) f32 delta, this rank's rows; null if packed / all-zero
+    std::vector<std::array<float*, P_COUNT>> raw;
     std::vector<float*> norm1, norm2;  // device, effective
     float* final_norm = nullptr;
     float* embed_raw = nullptr;        // device [vocab x dim] or null
@@ -161,6 +163,9 @@ struct Plan {
     std::vector<void*> allocs;
     // per layer & group: delta units
     std::vector<std::array<std::vector<DeltaUnit>, 4>> units;  // qkv, o, gu, down
+    // raw projection deltas (serve.cpp:27-35): groups with any take the units path + raw pass
+    std::vector<std::array<std::vector<RawJob>, 4>> raw;
+    bool raw_group[4] = {false, false, false, false};
     std::vector<DeltaUnit> lm_units;
     GemmPlan g_qkv, g_o, g_gu, g_down, g_lm;
     CUtensorMap x_xn, x_ctx, x_act;  // B-operand maps for this batch size
@@ -643,6 +648,7 @@ struct PoolImpl {
     void load_tenant(Tenant& t, const std::vector<EntryView>& ev) {
         BD_CUDA(cudaSetDevice(device));
         t.proj.assign(a.n_layers, {});
+        t.raw.assign(a.n_layers, {});
         t.norm1.assign(a.n_layers, nullptr);
         t.norm2.assign(a.n_layers, nullptr);
         t.bytes = 0;
@@ -666,11 +672,21 @@ struct PoolImpl {
         for (uint64_t l = 0; l < a.n_layers; ++l) {
             for (int p = 0; p < P_COUNT; ++p) {
                 const EntryView& e = ev[1 + 9 * l + p];
-                require(e.packed && e.planes >= 1 && e.planes <= kMaxPlanesPerUnit, BD_ERR_BAD_ARGUMENT,
-                        "delta '" + t.id + "': tensor '" + tname(1 + 9 * l + p) +
-                            "' must be packed with 1-4 planes for the device engine");
                 uint64_t r0, nr;
                 local_rows(p, r0, nr);
+                t.raw[l][p] = nullptr;
+                if (!e.packed) {  // raw projection delta: resident in f32 (memory_report's 4 B/param)
+                    if (e.raw) {
+                        float* d = dmalloc<float>(nr * e.cols, &t.allocs);
+                        BD_CUDA(cudaMemcpy(d, e.raw + r0 * e.cols, nr * e.cols * 4,
+                                           e.is_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+                        t.raw[l][p] = d;
+                    }
+                    continue;
+                }
+                require(e.planes >= 1 && e.planes <= kMaxPlanesPerUnit, BD_ERR_BAD_ARGUMENT,
+                        "delta '" + t.id + "': tensor '" + tname(1 + 9 * l + p) +
+                            "' has more than 4 planes (the device engine's limit)");
                 t.proj[l][p] = upload_planes(t, e, r0, nr);
             }
             std::vector<float> n1 = base_norm1[l], n2 = base_norm2[l];
@@ -830,6 +846,7 @@ struct PoolImpl {
                                   {{P_DOWN}, a.intermediate, ld_inter}};
         for (int gi = 0; gi < 4; ++gi) {
             const GroupDef& gd = defs[gi];
+            if (p.raw_group[gi]) continue;  // raw projection deltas: units path
             int seg_rows[kLutMaxSegs];
             for (size_t s = 0; s < gd.projs.size(); ++s) {
                 uint64_t r0, nr;
@@ -880,6 +897,7 @@ struct PoolImpl {
                                   {{P_DOWN}, a.intermediate, ld_inter}};
         for (int gi = 0; gi < 4; ++gi) {
             const GroupDef& gd = defs[gi];
+            if (p.raw_group[gi]) continue;  // raw projection deltas: units path
             int seg_rows[kLutMaxSegs];
             for (size_t s2 = 0; s2 < gd.projs.size(); ++s2) {
                 uint64_t r0, nr;
@@ -962,7 +980,7 @@ struct PoolImpl {
         p.mt4.assign(nL, {});
         for (int gi = 0; gi < 4; ++gi) {
             const GroupDef& gd = defs[gi];
-            if (gd.cols % 128) continue;
+            if (gd.cols % 128 || p.raw_group[gi]) continue;
             bool ok = true;
             uint64_t M = 0;
             std::vector<int> sub_row0;
@@ -1102,6 +1120,7 @@ struct PoolImpl {
                     for (int pj : projs) {
                         DeltaUnit u{};
                         const auto& planes = tenants[t].proj[l][pj];
+                        if (planes.empty()) continue;  // raw projection delta (raw pass)
                         u.n_planes = int(planes.size());
                         for (size_t k = 0; k < planes.size(); ++k) {
                             u.bits[k] = planes[k].bits;
@@ -1125,6 +1144,32 @@ struct PoolImpl {
             p->units[l][1] = units_for({P_O}, l);
             p->units[l][2] = units_for({P_GATE, P_UP}, l);
             p->units[l][3] = units_for({P_DOWN}, l);
+        }
+        // raw projection deltas: one job per (tenant, projection, <= kRawMaxReq requests)
+        {
+            const std::vector<int> gp[4] = {{P_Q, P_K, P_V}, {P_O}, {P_GATE, P_UP}, {P_DOWN}};
+            p->raw.assign(nL, {});
+            for (uint64_t l = 0; l < nL; ++l)
+                for (int gi = 0; gi < 4; ++gi)
+                    for (int pj : gp[gi])
+                        for (int t : order) {
+                            const Tenant& tn = tenants[t];
+                            if (!tn.proj[l][pj].empty()) continue;
+                            p->raw_group[gi] = true;  // raw entry (null: all zero, no job)
+                            if (!tn.raw[l][pj]) continue;
+                            const auto& rq = by_t[t];
+                            uint64_t r0, nr;
+                            local_rows(pj, r0, nr);
+                            for (size_t c = 0; c < rq.size(); c += kRawMaxReq) {
+                                RawJob j{};
+                                j.W = tn.raw[l][pj];
+                                j.row0 = int(stack_offset(pj));
+                                j.rows = int(nr);
+                                j.n_req = int(std::min<size_t>(kRawMaxReq, rq.size() - c));
+                                for (int q = 0; q < j.n_req; ++q) j.req[q] = rq[c + q];
+                                p->raw[l][gi].push_back(j);
+                            }
+                        }
         }
         for (int t : order) {
             const auto& rq = by_t[t];
@@ -1318,6 +1363,8 @@ struct PoolImpl {
         prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm(g, l, group, mw, mx, s); });
         prof(BD_PROF_DELTA_QKV + group, s, [&] {
             delta_units_launch(units.data(), int(units.size()), X, ldx, cols, B, D, int(g.M), s);
+            const auto& rj = p.raw[l][group];
+            if (!rj.empty()) raw_delta_launch(rj.data(), int(rj.size()), X, ldx, cols, D, int(g.M), s);
         });
     }
 

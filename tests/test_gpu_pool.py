@@ -423,3 +423,62 @@ def test_int8_backbone_toy_matches_port(cuda, toy, port):
     assert dense.resident_bytes() - pool.resident_bytes() == 4 * proj - (proj + 4 * rows)
     pool.close()
     dense.close()
+
+
+def test_raw_projection_deltas_match_port(cuda, port):
+    """Raw (unquantised f32) projection deltas (build_delta_file with a policy that leaves a
+    projection raw; apply_delta_correction's dense branch, P:src/serve.cpp:27-35) next to
+    packed ones: three tenants, one all-packed, one with raw o / down, one with raw q / gate
+    (and an all-zero raw k), against the port at the bf16 tolerance. The raw groups run the
+    units path + raw pass, the all-packed groups the default dispatch."""
+    arch = dict(vocab=64, dim=256, n_layers=2, n_heads=2, intermediate=512, max_seq=32,
+                rope_theta=10000.0, kv_dim=128)
+    rng = np.random.default_rng(11)
+    tens = {}
+    for name, r, c in tensor_shapes(arch):
+        w = rng.standard_normal((r, c)).astype(np.float32) * (1.0 if r == 1 else 0.05)
+        tens[name] = bf16_round(w + (1.0 if r == 1 else 0.0))
+    pool = ServingPool(arch, tens)
+    ents = [_random_entries(arch, rng) for _ in range(3)]
+    raw_of = {1: ("layers.0.attn_o", "layers.1.mlp_down"),
+              2: ("layers.0.attn_q", "layers.1.mlp_gate", "layers.1.attn_k")}
+    for t, names in raw_of.items():
+        for i, (n, r, c) in enumerate(tensor_shapes(arch)):
+            if n in names:
+                raw = None if n == "layers.1.attn_k" else (rng.standard_normal((r, c)) * 1e-2).astype(np.float32)
+                ents[t][i] = dict(name=n, kind="raw", rows=r, cols=c, raw=raw)
+        assert sum(e["kind"] == "raw" and e["rows"] > 1 and "layers" in e["name"] for e in ents[t]) == len(names)
+    for t, e in enumerate(ents):
+        pool.register_delta_entries(f"t{t}", e)
+    rids = [pool.open_request(f"t{t % 3}") for t in range(5)]
+    names = [n for n, _, _ in tensor_shapes(arch)]
+    port_ents = []
+    for es in ents:
+        pe = []
+        for e in es:
+            e2 = dict(e)
+            if e2["kind"] == "raw":
+                r2 = e2["raw"]
+                e2["raw"] = (np.zeros(e2["rows"] * e2["cols"], np.float32) if r2 is None else r2.reshape(-1))
+            pe.append(e2)
+        port_ents.append(pe)
+    # sensitivity: the same tenants with the raw projection deltas dropped
+    no_raw = [[dict(e, raw=np.zeros_like(e["raw"])) if e["kind"] == "raw" and e["rows"] > 1
+               and "layers" in e["name"] else e for e in es] for es in port_ents]
+    flat = np.concatenate([tens[n].reshape(-1) for n in names])
+    kc = [np.zeros((2, arch["max_seq"], arch["kv_dim"]), np.float32) for _ in range(5)]
+    vc = [np.zeros_like(k) for k in kc]
+    kc2 = [k.copy() for k in kc]
+    vc2 = [v.copy() for v in vc]
+    for pos in range(6):
+        toks = [int(x) for x in rng.integers(0, arch["vocab"], 5)]
+        got = pool.decode_step([(r, toks[i], pos) for i, r in enumerate(rids)])
+        want = port.decode(arch, flat, port_ents, [i % 3 for i in range(5)], toks, [pos] * 5, kc, vc)
+        want0 = port.decode(arch, flat, no_raw, [i % 3 for i in range(5)], toks, [pos] * 5, kc2, vc2)
+        for i in range(5):
+            # bf16 backbone activations against the f32 port: the head_dim-128 tolerance
+            err = rel_l2(got[i], want[i])
+            assert err <= 2e-2, (pos, i, err)
+            if i % 3:  # tenants with raw projections: dropping them is well outside tolerance
+                assert rel_l2(want0[i], want[i]) > 2 * 2e-2, (pos, i)
+    pool.close()
