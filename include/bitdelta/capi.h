@@ -229,10 +229,10 @@ int bd_pool_register_delta_file(bd_pool* pool, const char* id, const char* path,
 
 /* Host-only check of a .bdelta container (read_delta_file's validation, delta.cpp:265-334,
  * no device needed): *n_tensors = entries, *n_packed = packed entries, *max_planes = the
- * largest plane count. The pool serves packed projections with 1..4 planes per projection
- * and raw (f32) entries anywhere, projections included (a group with a raw projection delta
- * takes the generic delta units + raw pass for that step); > 4 planes are rejected by
- * register_delta with BD_ERR_BAD_ARGUMENT (the reference's ServingPool would serve them). */
+ * largest plane count. The pool serves packed projections with 1..32 planes and raw (f32)
+ * entries anywhere, projections included (a group with a raw projection delta or more than 4
+ * planes takes the generic delta units + extra passes for that step); a packed lm_head has
+ * at most 4 planes (BD_ERR_BAD_ARGUMENT otherwise). */
 int bd_bdelta_validate(const char* path, uint64_t* n_tensors, uint64_t* n_packed, uint64_t* max_planes);
 
 int bd_pool_open_request(bd_pool* pool, const char* delta_id, uint64_t* request_id);

@@ -74,6 +74,7 @@ void dot_f64_launch(const float* a, const float* b, uint64_t n, double* acc, cud
 // requests req[0..n_req). Output d[b][row] = sum over units of alpha * S x_b.
 constexpr int kMaxReqPerUnit = 4;
 constexpr int kMaxPlanesPerUnit = 4;
+constexpr int kMaxPlanesPerTensor = 32;  // pool: planes beyond 4 run as accumulate passes
 struct DeltaUnit {
     const uint8_t* bits[kMaxPlanesPerUnit];  // reference layout of one [rows x cols] plane each
     float alpha[kMaxPlanesPerUnit];
@@ -82,9 +83,11 @@ struct DeltaUnit {
     int32_t n_req;
     int32_t req[kMaxReqPerUnit];
 };
-// X: bf16 [batch x ldx] activations; D: f32 [batch x out_rows] (zeroed here)
+// X: bf16 [batch x ldx] activations; D: f32 [batch x out_rows] (zeroed here, or added to with
+// accumulate: a projection's planes beyond the first kMaxPlanesPerUnit, in a later launch)
 void delta_units_launch(const DeltaUnit* units_host, int n_units, const void* X, int ldx,
-                        int cols, int batch, float* D, int out_rows, cudaStream_t stream);
+                        int cols, int batch, float* D, int out_rows, cudaStream_t stream,
+                        bool accumulate = false);
 
 // ---- raw (unquantised f32) projection deltas, P:src/serve.cpp:27-35 (packed.cu) ----
 // D[req][row0 + r] += sum_k W[r][k] x_req[k] for the job's requests (after the units pass,

@@ -88,6 +88,7 @@ struct UnitTable {
     int n_units;
     int cols, ldx, batch, out_rows;
     int rows_per_block;
+    int accumulate;                      // D += (units of a projection's planes 5, 6, ...)
     int block0[kMaxUnitsPerLaunch + 1];  // prefix of row-blocks per unit
     DeltaUnit u[kMaxUnitsPerLaunch];
 };
@@ -154,7 +155,8 @@ __global__ void __launch_bounds__(kDuThreads)
         }
         if (lane == 0)
             for (int q = 0; q < nq; ++q)
-                D[static_cast<size_t>(u.req[q]) * tab.out_rows + u.row0 + r] = tot[q];
+                D[static_cast<size_t>(u.req[q]) * tab.out_rows + u.row0 + r] =
+                    tab.accumulate ? D[static_cast<size_t>(u.req[q]) * tab.out_rows + u.row0 + r] + tot[q] : tot[q];
     }
 }
 
@@ -374,8 +376,8 @@ void raw_delta_launch(const RawJob* jobs, int n_jobs, const void* X, int ldx, in
 }
 
 void delta_units_launch(const DeltaUnit* units, int n_units, const void* X, int ldx, int cols,
-                        int batch, float* D, int out_rows, cudaStream_t stream) {
-    BD_CUDA(cudaMemsetAsync(D, 0, static_cast<size_t>(batch) * out_rows * sizeof(float), stream));
+                        int batch, float* D, int out_rows, cudaStream_t stream, bool accumulate) {
+    if (!accumulate) BD_CUDA(cudaMemsetAsync(D, 0, static_cast<size_t>(batch) * out_rows * sizeof(float), stream));
     if (n_units == 0) return;
     const int nchunk = (cols + 31) / 32;
     static bool attr = false;
@@ -393,6 +395,7 @@ void delta_units_launch(const DeltaUnit* units, int n_units, const void* X, int 
         tab.batch = batch;
         tab.out_rows = out_rows;
         tab.rows_per_block = 64;
+        tab.accumulate = accumulate ? 1 : 0;
         int blocks = 0, max_q = 1;
         for (int i = 0; i < cnt; ++i) {
             tab.u[i] = units[first + i];

@@ -163,8 +163,10 @@ struct Plan {
     std::vector<void*> allocs;
     // per layer & group: delta units
     std::vector<std::array<std::vector<DeltaUnit>, 4>> units;  // qkv, o, gu, down
-    // raw projection deltas (serve.cpp:27-35): groups with any take the units path + raw pass
+    // raw projection deltas (serve.cpp:27-35) and planes beyond kMaxPlanesPerUnit: groups with
+    // any take the units path + these extra passes
     std::vector<std::array<std::vector<RawJob>, 4>> raw;
+    std::vector<std::array<std::vector<DeltaUnit>, 4>> units_x;  // planes 5, 6, ... (D +=)
     bool raw_group[4] = {false, false, false, false};
     std::vector<DeltaUnit> lm_units;
     GemmPlan g_qkv, g_o, g_gu, g_down, g_lm;
@@ -684,9 +686,8 @@ struct PoolImpl {
                     }
                     continue;
                 }
-                require(e.planes >= 1 && e.planes <= kMaxPlanesPerUnit, BD_ERR_BAD_ARGUMENT,
-                        "delta '" + t.id + "': tensor '" + tname(1 + 9 * l + p) +
-                            "' has more than 4 planes (the device engine's limit)");
+                require(e.planes >= 1 && e.planes <= kMaxPlanesPerTensor, BD_ERR_BAD_ARGUMENT,
+                        "delta '" + t.id + "': tensor '" + tname(1 + 9 * l + p) + "' has too many planes");
                 t.proj[l][p] = upload_planes(t, e, r0, nr);
             }
             std::vector<float> n1 = base_norm1[l], n2 = base_norm2[l];
@@ -1112,7 +1113,9 @@ struct PoolImpl {
             if (!by_t.count(t)) order.push_back(t);
             by_t[t].push_back(b);
         }
-        auto units_for = [&](std::initializer_list<int> projs, uint64_t l) {
+        // chunk c of a projection's planes (kMaxPlanesPerUnit each): c = 0 the main units,
+        // c >= 1 the accumulate passes
+        auto units_for = [&](std::initializer_list<int> projs, uint64_t l, int chunk = 0) {
             std::vector<DeltaUnit> out;
             for (int t : order) {
                 const auto& rq = by_t[t];
@@ -1121,10 +1124,12 @@ struct PoolImpl {
                         DeltaUnit u{};
                         const auto& planes = tenants[t].proj[l][pj];
                         if (planes.empty()) continue;  // raw projection delta (raw pass)
-                        u.n_planes = int(planes.size());
-                        for (size_t k = 0; k < planes.size(); ++k) {
-                            u.bits[k] = planes[k].bits;
-                            u.alpha[k] = planes[k].alpha;
+                        const int k0 = chunk * kMaxPlanesPerUnit;
+                        if (int(planes.size()) <= k0) continue;
+                        u.n_planes = std::min(kMaxPlanesPerUnit, int(planes.size()) - k0);
+                        for (int k = 0; k < u.n_planes; ++k) {
+                            u.bits[k] = planes[k0 + k].bits;
+                            u.alpha[k] = planes[k0 + k].alpha;
                         }
                         uint64_t r0, nr;
                         local_rows(pj, r0, nr);
@@ -1144,6 +1149,26 @@ struct PoolImpl {
             p->units[l][1] = units_for({P_O}, l);
             p->units[l][2] = units_for({P_GATE, P_UP}, l);
             p->units[l][3] = units_for({P_DOWN}, l);
+        }
+        // planes beyond kMaxPlanesPerUnit: accumulate passes, the group on the units path
+        p->units_x.assign(nL, {});
+        {
+            const std::vector<int> gp[4] = {{P_Q, P_K, P_V}, {P_O}, {P_GATE, P_UP}, {P_DOWN}};
+            for (uint64_t l = 0; l < nL; ++l)
+                for (int gi = 0; gi < 4; ++gi) {
+                    int max_planes = 0;
+                    for (int t : order)
+                        for (int pj : gp[gi]) max_planes = std::max(max_planes, int(tenants[t].proj[l][pj].size()));
+                    if (max_planes <= kMaxPlanesPerUnit) continue;
+                    p->raw_group[gi] = true;
+                    for (int c = 1; c * kMaxPlanesPerUnit < max_planes; ++c) {
+                        auto more = gi == 0 ? units_for({P_Q, P_K, P_V}, l, c)
+                                    : gi == 1 ? units_for({P_O}, l, c)
+                                    : gi == 2 ? units_for({P_GATE, P_UP}, l, c)
+                                              : units_for({P_DOWN}, l, c);
+                        p->units_x[l][gi].insert(p->units_x[l][gi].end(), more.begin(), more.end());
+                    }
+                }
         }
         // raw projection deltas: one job per (tenant, projection, <= kRawMaxReq requests)
         {
@@ -1363,6 +1388,26 @@ struct PoolImpl {
         prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm(g, l, group, mw, mx, s); });
         prof(BD_PROF_DELTA_QKV + group, s, [&] {
             delta_units_launch(units.data(), int(units.size()), X, ldx, cols, B, D, int(g.M), s);
+            // one launch per further plane chunk: a unit's rows are never written twice in one launch
+            const auto& ux = p.units_x[l][group];
+            for (size_t i0 = 0; i0 < ux.size();) {
+                size_t i1 = i0 + 1;  // the next run of units with no (request, row) overlap
+                auto overlaps = [&](const DeltaUnit& a2, const DeltaUnit& b2) {
+                    if (a2.row0 != b2.row0) return false;
+                    for (int x = 0; x < a2.n_req; ++x)
+                        for (int y = 0; y < b2.n_req; ++y)
+                            if (a2.req[x] == b2.req[y]) return true;
+                    return false;
+                };
+                while (i1 < ux.size()) {
+                    bool clash = false;
+                    for (size_t k = i0; k < i1 && !clash; ++k) clash = overlaps(ux[k], ux[i1]);
+                    if (clash) break;
+                    ++i1;
+                }
+                delta_units_launch(ux.data() + i0, int(i1 - i0), X, ldx, cols, B, D, int(g.M), s, true);
+                i0 = i1;
+            }
             const auto& rj = p.raw[l][group];
             if (!rj.empty()) raw_delta_launch(rj.data(), int(rj.size()), X, ldx, cols, D, int(g.M), s);
         });

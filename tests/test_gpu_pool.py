@@ -482,3 +482,50 @@ def test_raw_projection_deltas_match_port(cuda, port):
             if i % 3:  # tenants with raw projections: dropping them is well outside tolerance
                 assert rel_l2(want0[i], want[i]) > 2 * 2e-2, (pos, i)
     pool.close()
+
+
+def test_more_than_four_planes_match_port(cuda, port):
+    """compress_stack with k > 4 (P:src/delta.cpp:57-70): planes beyond the engine's 4 per
+    unit run as accumulate passes of the delta units; 6- and 9-plane projections next to
+    1-plane ones, against the port (which sums every plane like apply_delta_correction)."""
+    arch = dict(vocab=64, dim=256, n_layers=2, n_heads=2, intermediate=512, max_seq=32,
+                rope_theta=10000.0, kv_dim=128)
+    rng = np.random.default_rng(12)
+    tens = {}
+    for name, r, c in tensor_shapes(arch):
+        w = rng.standard_normal((r, c)).astype(np.float32) * (1.0 if r == 1 else 0.05)
+        tens[name] = bf16_round(w + (1.0 if r == 1 else 0.0))
+    pool = ServingPool(arch, tens)
+    ents = [_random_entries(arch, rng) for _ in range(2)]
+    wide = {"layers.0.attn_v": 6, "layers.1.mlp_up": 9, "layers.1.mlp_down": 5}
+    for i, (n, r, c) in enumerate(tensor_shapes(arch)):
+        if n in wide:
+            k, nb = wide[n], (r * c + 7) // 8
+            ents[1][i] = dict(name=n, kind="packed", rows=r, cols=c,
+                              bits=rng.integers(0, 256, (k, nb), dtype=np.uint8),
+                              scales=(6e-3 * 0.9 ** np.arange(k)).astype(np.float32))
+    for t, e in enumerate(ents):
+        pool.register_delta_entries(f"t{t}", e)
+    rids = [pool.open_request(f"t{t % 2}") for t in range(4)]
+    names = [n for n, _, _ in tensor_shapes(arch)]
+    port_ents = [[dict(e, raw=e["raw"].reshape(-1)) if e["kind"] == "raw" else e for e in es] for es in ents]
+    # sensitivity: the same tenants with the planes beyond the 4th dropped
+    cut = [[dict(e, bits=e["bits"][:4], scales=e["scales"][:4]) if e["kind"] == "packed" else e for e in es]
+           for es in port_ents]
+    flat = np.concatenate([tens[n].reshape(-1) for n in names])
+    kc = [np.zeros((2, arch["max_seq"], arch["kv_dim"]), np.float32) for _ in range(4)]
+    vc = [np.zeros_like(k) for k in kc]
+    kc2, vc2 = [k.copy() for k in kc], [v.copy() for v in vc]
+    worst_cut = 0.0
+    for pos in range(6):
+        toks = [int(x) for x in rng.integers(0, arch["vocab"], 4)]
+        got = pool.decode_step([(r, toks[i], pos) for i, r in enumerate(rids)])
+        want = port.decode(arch, flat, port_ents, [i % 2 for i in range(4)], toks, [pos] * 4, kc, vc)
+        want4 = port.decode(arch, flat, cut, [i % 2 for i in range(4)], toks, [pos] * 4, kc2, vc2)
+        for i in range(4):
+            err = rel_l2(got[i], want[i])
+            assert err <= 2e-2, (pos, i, err)  # bf16 activations vs the f32 port (head_dim 128)
+            if i % 2:
+                worst_cut = max(worst_cut, rel_l2(want4[i], want[i]))
+    assert worst_cut > 2 * 2e-2, worst_cut  # dropping the extra planes is well outside tolerance
+    pool.close()
