@@ -27,7 +27,6 @@
 #include <mutex>
 
 #include "common.cuh"
-#include "fuse.cuh"
 #include "kernels.h"
 
 namespace bd {
@@ -57,31 +56,12 @@ __host__ __device__ inline GemmSmemLayout gemm_layout(int bn, int stages) {
 // RTN tensor, X holds kPieces int8 pieces per request (quant_pieces_kernel), the MMA is
 // kind::i8 (s8 x s8 -> exact s32) with K = 128 per 128-byte stage row, and the epilogue
 // recombines y = row_scale[m] * float(sum_p acc_p * piece_scale_p).
-// Fused epilogue (fuse.cuh), after every role of the CTA is done: arrive; the waiter (K2 of
-// a fused group) waits for every producer and runs tiles x requests over all 8 warps of all
-// CTAs. Not inlined: the kernel keeps its register budget.
-static __device__ __noinline__ void gemm_fz_epilogue(const TileFuse& fz) {
-    if (threadIdx.x == 0) fz_producer_arrive(fz);
-    if (!fz.waiter) return;
-    if (threadIdx.x == 0) fz_wait_all(fz);
-    __syncthreads();
-    __threadfence();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const int items = fz.tiles * fz.B;
-    for (int k = blockIdx.x * nw + warp; k < items; k += gridDim.x * nw) fz_tile_warp(fz, k / fz.B, k % fz.B, lane);
-    __syncthreads();
-    if (threadIdx.x == 0) fz_depart(fz);
-}
-
-// <= 64 registers per thread (as if 4 CTAs per SM): a GEMM CTA must fit beside a K3 LUT CTA
-// (512 threads x 96 registers)
 template <bool kI8>
-__global__ void __launch_bounds__(kGemmThreads, 4)
+__global__ void __launch_bounds__(kGemmThreads, 1)
     base_gemm_kernel(const __grid_constant__ CUtensorMap map_w,
                      const __grid_constant__ CUtensorMap map_x, float* __restrict__ partial,
                      int M, int N_valid, int bn, int kb_total, int kb_per_split, int splits, int n_units,
-                     int stages, const float* __restrict__ row_scale, const float* __restrict__ piece_scale,
-                     const __grid_constant__ TileFuse fz) {
+                     int stages, const float* __restrict__ row_scale, const float* __restrict__ piece_scale) {
     extern __shared__ uint8_t smem_raw[];
     const unsigned long long t_entry = gtimer();
     unsigned long long t_wait = 0;
@@ -238,11 +218,9 @@ __global__ void __launch_bounds__(kGemmThreads, 4)
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_free[acc]);
         }
-        if (fz.kind) __threadfence();  // this thread's partial stores, before the arrival
     }
     tc_fence_before();
     __syncthreads();
-    if (fz.kind) gemm_fz_epilogue(fz);
     if (warp == 2) {
         if (acc_cols == 32) tmem_dealloc<64>(taddr);
         else if (acc_cols == 64) tmem_dealloc<128>(taddr);
@@ -353,8 +331,7 @@ GemmPlan plan_gemm(uint64_t M, uint64_t K, int batch, int smem_cap, bool i8) {
 
 template <bool kI8>
 static void gemm_launch_t(const GemmPlan& p, const CUtensorMap& map_w, const CUtensorMap& map_x,
-                          float* partial, const float* row_scale, const float* piece_scale, cudaStream_t stream,
-                          const TileFuse& fz = TileFuse{}) {
+                          float* partial, const float* row_scale, const float* piece_scale, cudaStream_t stream) {
     static bool attr_set = false;
     if (!attr_set) {
         BD_CUDA(cudaFuncSetAttribute(base_gemm_kernel<kI8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -368,16 +345,15 @@ static void gemm_launch_t(const GemmPlan& p, const CUtensorMap& map_w, const CUt
     const int n_units = p.m_tiles * p.splits;
     BD_CUDA(launch_pdl(base_gemm_kernel<kI8>, dim3(std::min(n_units, p.grid)), dim3(kGemmThreads), size_t(p.smem),
                        stream, map_w, map_x, partial, int(p.M), p.batch, p.bn, p.kb_total, p.kb_per_split, p.splits,
-                       n_units, p.stages, row_scale, piece_scale, fz));
+                       n_units, p.stages, row_scale, piece_scale));
     note_launch();
     BD_CUDA(cudaGetLastError());
 }
 
 void base_gemm_launch(const GemmPlan& p, const CUtensorMap& map_w, const CUtensorMap& map_x,
-                      float* partial, cudaStream_t stream, const TileFuse* fz) {
+                      float* partial, cudaStream_t stream) {
     require(!p.i8, BD_ERR_BAD_ARGUMENT, "base gemm: int8 plan on the bf16 kernel");
-    require(!fz || !fz->kind || p.M % kBM == 0, BD_ERR_BAD_ARGUMENT, "base gemm: fused epilogue needs M % 128 == 0");
-    gemm_launch_t<false>(p, map_w, map_x, partial, nullptr, nullptr, stream, fz ? *fz : TileFuse{});
+    gemm_launch_t<false>(p, map_w, map_x, partial, nullptr, nullptr, stream);
 }
 
 void i8_gemm_launch(const GemmPlan& p, const CUtensorMap& map_wq, const CUtensorMap& map_xq,

@@ -14,7 +14,6 @@
 #include <cstdlib>
 
 #include "common.cuh"
-#include "fuse.cuh"
 #include "glue.h"
 
 namespace bd {
@@ -540,24 +539,12 @@ __global__ void __launch_bounds__(kA2Threads)
     griddep_wait();  // PDL: q/k/v partials come from the previous kernel
     const unsigned long long t_wait = gtimer();
 
-    // fused norm1 (TileFuse): q/k/v were computed from x * w_b, the RMS scale r_b applies here
-    double rinv = 1.0;
-    if (a.msq) {
-        __shared__ double rinv_s;
-        if (threadIdx.x < 32) {
-            const double r = fz_rinv(a.msq, a.msq_tiles, a.msq_dim, b, int(threadIdx.x));
-            if (threadIdx.x == 0) rinv_s = r;
-        }
-        __syncthreads();
-        rinv = rinv_s;
-    }
     // q, k, v of this step (split-K + tenant delta), RoPE (same as attn_kernel)
     const float2* rope = a.rope + static_cast<size_t>(pos) * half;
     for (int i = threadIdx.x; i < 3 * hd; i += kA2Threads) {
         const int which = i / hd, d = i - which * hd;
         const int col = which == 0 ? h * hd + d : (which == 1 ? a.dim + kh * hd + d : a.dim + a.kv_dim + kh * hd + d);
-        float v = proj_val(qkv, b, col);
-        if (a.msq) v = static_cast<float>(static_cast<double>(v) * rinv);
+        const float v = proj_val(qkv, b, col);
         (which == 0 ? qs : (which == 1 ? ks : vs))[d] = which == 2 ? bf16_to_f32(f32_to_bf16(v)) : v;
     }
     __syncthreads();
@@ -766,22 +753,7 @@ bool proj_vec4_ok(const ProjOut& p) {
     return p.M % 4 == 0 && p.col0 % 4 == 0 && p.pstride % 4 == 0 && reinterpret_cast<uintptr_t>(p.P) % 16 == 0 &&
            (!p.D || (p.dstride % 4 == 0 && reinterpret_cast<uintptr_t>(p.D) % 16 == 0));
 }
-// kind-1 tiles on their own (the first layer's norm1): one CTA per tile, warp w -> requests
-// w, w + 4, ...
-__global__ void __launch_bounds__(128) fuse_norm_kernel(const __grid_constant__ TileFuse f) {
-    if (BD_PDL_EARLY) griddep_launch_dependents();  // next linear's prologue may start
-    griddep_wait();
-    const int t = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int b = w; b < f.B; b += 4) fz_tile_warp(f, t, b, lane);
-}
 }  // namespace
-
-void fuse_norm_launch(const TileFuse& f, cudaStream_t s) {
-    require(f.kind == 1 && f.dim % 128 == 0 && f.tiles == f.dim / 128, BD_ERR_BAD_ARGUMENT, "fuse_norm: bad tiles");
-    BD_CUDA(launch_pdl(fuse_norm_kernel, dim3(f.tiles), dim3(128), 0, s, f));
-    note_launch();
-    BD_CUDA(cudaGetLastError());
-}
 
 size_t norm_ws_bytes(int batch, int dim) {
     const size_t cnt = (size_t(batch) * sizeof(unsigned) + 255) / 256 * 256;
@@ -848,7 +820,6 @@ void attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int 
         BD_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    require(!a.msq, BD_ERR_BAD_ARGUMENT, "attention: the fused norm scale needs head_dim 128");
     attn_kernel<<<dim3(a.n_heads, batch), kAttnThreads, smem, s>>>(qkv, a, pos_dev, ctx, ld_ctx);
     note_launch();
     BD_CUDA(cudaGetLastError());

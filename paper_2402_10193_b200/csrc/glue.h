@@ -22,44 +22,6 @@ struct ProjOut {
     int g_cols = 0, g_batch = 0;
 };
 
-// Fused step epilogues (fuse.cuh): the residual + RMSNorm after the o / down projections and
-// the SiLU after gate/up run inside the projection kernels instead of their own launches.
-// Every producer CTA (K2, the K3 LUT) arrives on the group's counter after its partial
-// stores; the K2 CTAs (the waiter) wait for all arrivals, then run the
-// 128-row output tiles (tile t: rows [128 t, 128 t + 128), gate/up: and the same rows of up
-// at + fold) for every request, spread over all of their warps:
-//   kind 1 (residual + norm, serve.cpp:283-293): x += proj; xn = bf16(x * w_b);
-//          msq_out[b][t] = sum over the tile of double(x)^2
-//   kind 2 (SiLU, serve.cpp:301-302): act = bf16(silu(r_b g) * (r_b u)) with r_b from msq_in
-// RMSNorm's scale r_b = 1 / sqrt(mean x^2 + 1e-12) is a per-request scalar, so it moves to the
-// consumers of the following projection (W (r x) = r (W x)): attention scales q / k / v by
-// r_b (AttnArgs::msq), kind 2 scales gate / up.
-struct TileFuse {
-    int kind = 0;  // 0 = none
-    unsigned* cnt = nullptr;  // [0] arrivals, [32] departures (0 between phases)
-    unsigned arrivals = 0;    // producer CTAs of the group (K2 + every LUT launch)
-    int waiter = 0;           // this launch waits for every producer and runs the tiles (K2)
-    int tiles = 0, fold = 0, B = 0;
-    ProjOut src;  // the projection's partials
-    // kind 1
-    float* x = nullptr;
-    int dim = 0;
-    const float* const* norm_w = nullptr;  // [B] per-request norm rows (base + tenant delta)
-    uint16_t* xn = nullptr;
-    int ldxn = 0;
-    double* msq_out = nullptr;  // [B][tiles]
-    // kind 2
-    const double* msq_in = nullptr;  // [B][msq_tiles] from the kind-1 tiles of the norm
-    int msq_tiles = 0, msq_dim = 0;
-    uint16_t* act = nullptr;
-    int ld_act = 0;
-};
-struct LutParams;
-bool lut_fusable(const LutParams& p);
-size_t lut2_smem_bytes();
-// kind-1 tiles as a launch of their own (the first layer's norm1: no producer kernel)
-void fuse_norm_launch(const TileFuse& f, cudaStream_t s);
-
 // [world][batch][n_l] f32 partial sums of a row-sharded projection -> dst [batch][n_l]
 void shard_reduce_launch(const ProjOut& p, int batch, int n_l, float* dst, cudaStream_t s);
 // all-gathered [world][batch][n_l] bf16 -> [batch][ld] (columns r*n_l + i)
@@ -71,8 +33,6 @@ struct AttnArgs {
     uint16_t* const* kcache;  // per request: [n_layers][max_seq][kv_dim] bf16
     uint16_t* const* vcache;
     const float2* rope;       // [max_seq][hd/2] (cos, sin)
-    const double* msq = nullptr;  // fused norm1 (TileFuse kind 1): q/k/v *= r_b
-    int msq_tiles = 0, msq_dim = 0;
 };
 
 // ws: norm_ws_bytes(batch, dim) bytes, zeroed once at allocation (arrival counters

@@ -33,9 +33,8 @@ CUtensorMap make_tmap_2d(const void* ptr, CUtensorMapDataType dt, uint32_t elem_
 CUtensorMap tmap_weights(const void* W, uint64_t M, uint64_t K, uint64_t ld);
 CUtensorMap tmap_acts(const void* X, int batch, uint64_t K, uint64_t ld, int bn);
 // partial: [splits][batch][M] f32
-struct TileFuse;
 void base_gemm_launch(const GemmPlan& p, const CUtensorMap& map_w, const CUtensorMap& map_x,
-                      float* partial, cudaStream_t stream, const TileFuse* fz = nullptr);
+                      float* partial, cudaStream_t stream);
 // ---- K2 int8 (int8_matmul_nt, P:src/int8.cpp:67-81) ----
 // Wq: int8 [M x K] (row stride ld bytes, % 16 == 0); Xq: kPieces rows per request
 CUtensorMap tmap_weights_i8(const void* Wq, uint64_t M, uint64_t K, uint64_t ld);
@@ -166,9 +165,7 @@ struct LutParams {
 // Fills the geometry (slices, persistent grid) for the stacked rows; false if unsupported.
 bool plan_lut(LutParams& p, const int* seg_rows, int n_segs, int cols, int ldx, int batch);
 // out: [slices][batch][M] f32, alpha already applied; every (slice, req, row) of a job written
-struct TileFuse;
-void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream,
-                const TileFuse* fz = nullptr);
+void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream);
 
 // ---- K3d: tenants with many requests, dense tensor-core delta (mtd.cu) ----
 constexpr int kMtdMaxTenants = 8;

@@ -23,7 +23,6 @@
 #include <type_traits>
 
 #include "common.cuh"
-#include "fuse.cuh"
 #include "kernels.h"
 
 namespace bd {
@@ -259,7 +258,7 @@ __device__ __forceinline__ void build_tables_v2(float* T, const float* xs, int t
 template <int kWPR>  // words per plane row (cols/32); 0 = runtime value
 __global__ void __maxnreg__(kLutRegs)
     lut2_kernel(const __grid_constant__ LutParams p, const uint16_t* __restrict__ X,
-                float* __restrict__ out, const __grid_constant__ TileFuse fz) {
+                float* __restrict__ out) {
     extern __shared__ float T[];   // [128 KB tables][x of the slice, padded every 128]
     float* xs = T + kTableBytes / 4;
     const unsigned long long t_entry = gtimer();
@@ -406,11 +405,6 @@ __global__ void __maxnreg__(kLutRegs)
         }
         g += rb - ra;
     }
-    if (fz.kind) {  // fused epilogue (fuse.cuh): arrive once this CTA's partials are stored
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) fz_producer_arrive(fz);
-    }
     if (tracing()) {
         __syncthreads();
         if (threadIdx.x == 0) trace_rec(TR_LUT, t_entry, t_wait);
@@ -466,7 +460,7 @@ void lut_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t st
 }
 
 template <int kWPR>
-void lut2_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t stream, const TileFuse& fz) {
+void lut2_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t stream) {
     static bool attr = false;
     if (!attr) {
         BD_CUDA(cudaFuncSetAttribute(lut2_kernel<kWPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -480,7 +474,7 @@ void lut2_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t s
         attr = true;
     }
     BD_CUDA(launch_pdl(lut2_kernel<kWPR>, dim3(p.grid), dim3(kLutThreads), kLut2Smem, stream, p,
-                       static_cast<const uint16_t*>(X), out, fz));
+                       static_cast<const uint16_t*>(X), out));
 }
 
 static bool lut2_ok(const LutParams& p) {
@@ -492,23 +486,15 @@ static bool lut2_ok(const LutParams& p) {
     return true;
 }
 
-bool lut_fusable(const LutParams& p) { return lut2_ok(p); }
-
-size_t lut2_smem_bytes() { return kLut2Smem; }
-
-void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream, const TileFuse* fz) {
-    const TileFuse none{};
-    const TileFuse& f = fz ? *fz : none;
-    require(!f.kind || (lut2_ok(p) && !f.waiter), BD_ERR_BAD_ARGUMENT,
-            "lut: fused epilogue needs the v2 kernel and never waits");
+void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream) {
     if (lut2_ok(p)) {
         switch (p.cols) {
-            case 4096: lut2_launch_t<128>(p, X, out, stream, f); break;
-            case 8192: lut2_launch_t<256>(p, X, out, stream, f); break;
-            case 11008: lut2_launch_t<344>(p, X, out, stream, f); break;
-            case 14336: lut2_launch_t<448>(p, X, out, stream, f); break;
-            case 28672: lut2_launch_t<896>(p, X, out, stream, f); break;
-            default: lut2_launch_t<0>(p, X, out, stream, f); break;
+            case 4096: lut2_launch_t<128>(p, X, out, stream); break;
+            case 8192: lut2_launch_t<256>(p, X, out, stream); break;
+            case 11008: lut2_launch_t<344>(p, X, out, stream); break;
+            case 14336: lut2_launch_t<448>(p, X, out, stream); break;
+            case 28672: lut2_launch_t<896>(p, X, out, stream); break;
+            default: lut2_launch_t<0>(p, X, out, stream); break;
         }
         note_launch();
         BD_CUDA(cudaGetLastError());

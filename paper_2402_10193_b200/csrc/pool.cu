@@ -197,12 +197,6 @@ struct Plan {
     uint8_t* xpk = nullptr;  // FP4 activation pieces + scales [B][chunks][kXpBlock]
     cudaGraphExec_t graph_layers = nullptr, graph_full = nullptr;
     uint64_t kernels_layers = 0, kernels_full = 0;
-    // fused step epilogues (TileFuse, glue.h): residual + norm in the o / down kernels, SiLU
-    // in the gate/up kernels (every layer's o, gate/up and down on the LUT beside K2)
-    bool fuse = false;
-    int fz_max = 0;                    // counters per group (max tiles)
-    unsigned* fz_cnt = nullptr;        // [3][64]: o, gate/up, down (TileFuse::cnt)
-    double *msq1 = nullptr, *msq2 = nullptr;  // [B][dim / 128] tile sums of squares
 };
 
 }  // namespace
@@ -258,7 +252,6 @@ struct PoolImpl {
     // auto | lut | mt4 | units; BD_DELTA forces one K3 variant (test hook: every variant is
     // checked against the oracle on the same inputs)
     std::string delta_mode = "auto";
-    bool epi_fuse = true;  // fused step epilogues where the plan allows them (Plan::fuse)
 
     ~PoolImpl() {
         cudaSetDevice(device);
@@ -332,8 +325,6 @@ struct PoolImpl {
         BD_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         BD_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
         if (const char* e = std::getenv("BD_DELTA")) delta_mode = e;
-        // test / A-B hook: BD_EPI_FUSE=0 keeps the separate residual+norm and SiLU launches
-        if (const char* e = std::getenv("BD_EPI_FUSE")) epi_fuse = std::string(e) != "0";
 
         ld8_dim = round_up(a.dim, 16);
         ld8_inter = round_up(a.intermediate, 16);
@@ -1277,70 +1268,9 @@ struct PoolImpl {
                             "split-K workspace too small");
                 }
         }
-        plan_fuse(*p);
         auto& slot = plans[key];
         slot = std::move(p);
         return *slot;
-    }
-
-    // Fused step epilogues (Plan::fuse): every layer's o, gate/up and down groups on the LUT
-    // (v2) beside the bf16 K2, one rank, head_dim 128, 128-aligned dim / intermediate, and a
-    // K2 CTA fitting beside a LUT CTA on every SM (the waiting K2 CTAs spin while the LUT runs).
-    void plan_fuse(Plan& p) {
-        const uint64_t nL = a.n_layers;
-        p.fuse = epi_fuse && world == 1 && base_kind == 1 && hd == 128 && a.dim % 128 == 0 &&
-                 a.intermediate % 128 == 0 && a.kv_dim % 8 == 0 && !p.lut.empty();
-        for (uint64_t l = 0; l < nL && p.fuse; ++l)
-            for (int gi = 1; gi < 4 && p.fuse; ++gi) {
-                if (!lut_ok(p, l, gi) || mt4_ok(p, l, gi) || mtd_ok(p, l, gi)) p.fuse = false;
-                else
-                    for (const LutParams& lp : p.lut[l][gi].prm) p.fuse = p.fuse && lut_fusable(lp);
-            }
-        // K2 CTAs spin while the LUT drains: a LUT CTA must fit beside one on the SM
-        for (const GemmPlan* g : {&p.g_o, &p.g_gu, &p.g_down})
-            if (size_t(g->smem) + 1024 + lut2_smem_bytes() + 1024 > 228 * 1024) p.fuse = false;
-        if (!p.fuse) return;
-        const int B = p.B;
-        const int t_dim = int(a.dim / 128), t_inter = int(a.intermediate / 128);
-        p.fz_max = std::max(t_dim, t_inter);
-        p.fz_cnt = dmalloc<unsigned>(3 * 64, &p.allocs);  // per group: arrivals, departures (128 B apart)
-        BD_CUDA(cudaMemset(p.fz_cnt, 0, 3 * 64 * sizeof(unsigned)));
-        p.msq1 = dmalloc<double>(size_t(B) * t_dim, &p.allocs);
-        p.msq2 = dmalloc<double>(size_t(B) * t_dim, &p.allocs);
-    }
-    // K2's copy of a group's TileFuse: K2 waits for every producer and runs the tiles
-    const TileFuse* k2_fz(const TileFuse* fz) {
-        if (!fz) return nullptr;
-        fz_tmp = *fz;
-        fz_tmp.waiter = 1;
-        return &fz_tmp;
-    }
-    TileFuse fz_tmp;
-    // TileFuse of group k (0 = o, 1 = gate/up, 2 = down) of layer l
-    TileFuse tile_fuse(const Plan& p, uint64_t l, int k, const ProjOut& src, int norm_idx, double* msq_out,
-                       const double* msq_in) const {
-        TileFuse f;
-        f.kind = k == 1 ? 2 : 1;
-        f.cnt = p.fz_cnt + 64 * k;
-        const GemmPlan& g = k == 0 ? p.g_o : k == 1 ? p.g_gu : p.g_down;
-        f.arrivals = unsigned(std::min(g.m_tiles * g.splits, g.grid));  // K2 CTAs
-        for (const LutParams& lp : p.lut[l][k + 1].prm) f.arrivals += unsigned(lp.grid);
-        f.fold = k == 1 ? int(a.intermediate) : int(a.dim);
-        f.tiles = f.fold / 128;
-        f.B = p.B;
-        f.src = src;
-        f.x = x;
-        f.dim = int(a.dim);
-        f.norm_w = norm_idx >= 0 ? p.d_norm + size_t(norm_idx) * p.B : nullptr;
-        f.xn = xn;
-        f.ldxn = int(ld_dim);
-        f.msq_out = msq_out;
-        f.msq_in = msq_in;
-        f.msq_tiles = int(a.dim / 128);
-        f.msq_dim = int(a.dim);
-        f.act = act;
-        f.ld_act = int(ld_inter);
-        return f;
     }
 
     ProjOut proj_out(const GemmPlan& g, bool with_delta) const {
@@ -1404,16 +1334,14 @@ struct PoolImpl {
     // K2 for one projection group: the bf16 tcgen05 GEMM, or (int8 backbone) the kind::i8
     // GEMM against the pieces quant_pieces_launch wrote for this linear's input
     void base_gemm(const GemmPlan& g, uint64_t l, int group, const CUtensorMap& mw, const CUtensorMap& mx,
-                   cudaStream_t st, const TileFuse* fz = nullptr) {
-        require(!fz || !g.i8, BD_ERR_BAD_ARGUMENT, "fused epilogue on the int8 GEMM");
+                   cudaStream_t st) {
         if (g.i8) i8_gemm_launch(g, mw, mx, L[l].s8[group], xps, P, st);
-        else base_gemm_launch(g, mw, mx, P, st, fz);
+        else base_gemm_launch(g, mw, mx, P, st);
     }
 
     void linear(Plan& p, uint64_t l, int group, const GemmPlan& g, const CUtensorMap& mw,
                 const CUtensorMap& mx, const std::vector<DeltaUnit>& units, const uint16_t* X,
-                int ldx, int cols, int B, cudaStream_t s, const TileFuse* fz = nullptr) {
-        require(!fz || lut_ok(p, l, group), BD_ERR_BAD_ARGUMENT, "fused epilogue off the LUT path");
+                int ldx, int cols, int B, cudaStream_t s) {
         if (g.i8) {
             // the pieces buffer is free: the previous linear's K2 joined stream s before its
             // consumer ran
@@ -1443,20 +1371,18 @@ struct PoolImpl {
                 prof(BD_PROF_FUSED_QKV + group, s, [&] {
                     BD_CUDA(cudaEventRecord(ev_fork, s));
                     BD_CUDA(cudaStreamWaitEvent(stream2, ev_fork, 0));
-                    for (const LutParams& lp : luts) lut_launch(lp, X, D, s, fz);
-                    base_gemm(g, l, group, mw, mx, stream2, k2_fz(fz));
+                    for (const LutParams& lp : luts) lut_launch(lp, X, D, s);
+                    base_gemm(g, l, group, mw, mx, stream2);
                     BD_CUDA(cudaEventRecord(ev_join, stream2));
                     BD_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
                 });
                 return;
             }
-            // serial (profile_layers_serial): K2 and K3 timed on their own; with a fused
-            // epilogue the LUT first (K2 waits for its arrivals)
-            if (!fz) prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm(g, l, group, mw, mx, s); });
+            // serial (profile_layers_serial): K2 and K3 timed on their own
+            prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm(g, l, group, mw, mx, s); });
             prof(BD_PROF_DELTA_QKV + group, s, [&] {
-                for (const LutParams& lp : luts) lut_launch(lp, X, D, s, fz);
+                for (const LutParams& lp : luts) lut_launch(lp, X, D, s);
             });
-            if (fz) prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm(g, l, group, mw, mx, s, k2_fz(fz)); });
             return;
         }
         prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm(g, l, group, mw, mx, s); });
@@ -1537,30 +1463,13 @@ struct PoolImpl {
         AttnArgs aa{int(q_l), int(kv_l), int(a.n_heads / world), int(n_kv_heads / world), int(hd),
                     int(a.max_seq), 0, p.d_kc, p.d_vc, rope};
         ProjOut prev;  // pending residual contribution (previous layer's down)
-        // fused epilogues (Plan::fuse): norm1 of layer l > 0 runs in layer l - 1's down kernels,
-        // norm2 in the o kernels, SiLU in the gate/up kernels; the RMS scales of norm1 / norm2
-        // are applied by attention / the SiLU tiles (TileFuse, glue.h)
-        const bool fz = p.fuse;
-        if (fz) {
-            BD_CUDA(cudaMemsetAsync(p.fz_cnt, 0, 3 * 64 * sizeof(unsigned), s));
-            aa.msq = p.msq1;
-            aa.msq_tiles = int(a.dim / 128);
-            aa.msq_dim = int(a.dim);
-        }
         for (uint64_t l = 0; l < nL; ++l) {
             const LayerW& W = L[l];
             // x += down(prev); xn = norm1(x)   (x and xn replicated on every rank)
-            if (!fz) {
-                prof(BD_PROF_NORM, s, [&] {
-                    resid_norm_launch(x, B, int(a.dim), prev, p.d_norm + (2 * l) * B, xn, int(ld_dim),
-                                      nullptr, msq, s);
-                });
-            } else if (l == 0) {
-                prof(BD_PROF_NORM, s, [&] {
-                    TileFuse f = tile_fuse(p, 0, 0, ProjOut{}, 0, p.msq1, nullptr);
-                    fuse_norm_launch(f, s);
-                });
-            }
+            prof(BD_PROF_NORM, s, [&] {
+                resid_norm_launch(x, B, int(a.dim), prev, p.d_norm + (2 * l) * B, xn, int(ld_dim),
+                                  nullptr, msq, s);
+            });
             const bool i8 = base_kind == 2;
             linear(p, l, 0, p.g_qkv, i8 ? W.m8[0] : W.m_qkv, i8 ? p.xq_dim : p.x_xn, p.units[l][0], xn,
                    int(ld_dim), int(a.dim), B, s);
@@ -1570,18 +1479,6 @@ struct PoolImpl {
                             tp ? int(q_l) : int(ld_dim), s);
             });
             if (tp) exchange_bf16(ctx_loc, B, int(q_l), ctx, int(ld_dim), s);
-            if (fz) {
-                const TileFuse f_o = tile_fuse(p, l, 0, group_out(p, l, 1, p.g_o), int(2 * l + 1), p.msq2, nullptr);
-                linear(p, l, 1, p.g_o, W.m_o, p.x_ctx, p.units[l][1], ctx, int(ld_dim), int(a.dim), B, s, &f_o);
-                const TileFuse f_gu = tile_fuse(p, l, 1, group_out(p, l, 2, p.g_gu), -1, nullptr, p.msq2);
-                linear(p, l, 2, p.g_gu, W.m_gu, p.x_xn, p.units[l][2], xn, int(ld_dim), int(a.dim), B, s, &f_gu);
-                const bool last = l + 1 == nL;
-                const TileFuse f_dn = tile_fuse(p, l, 2, group_out(p, l, 3, p.g_down), int(2 * (l + 1)), p.msq1, nullptr);
-                linear(p, l, 3, p.g_down, W.m_down, p.x_act, p.units[l][3], act, int(ld_inter), int(a.intermediate), B,
-                       s, last ? nullptr : &f_dn);
-                prev = last ? group_out(p, l, 3, p.g_down) : ProjOut{};
-                continue;
-            }
             linear(p, l, 1, p.g_o, i8 ? W.m8[1] : W.m_o, i8 ? p.xq_dim : p.x_ctx, p.units[l][1], ctx,
                    int(ld_dim), int(a.dim), B, s);
             const ProjOut o_out = tp ? exchange_f32(group_out(p, l, 1, p.g_o), B, int(dim_l), s)
