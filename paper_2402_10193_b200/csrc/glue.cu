@@ -649,6 +649,159 @@ __global__ void __launch_bounds__(kA2Threads)
     if (threadIdx.x == 0) trace_rec(TR_ATTN, t_entry, t_wait);
 }
 
+// Grouped-query attention (kv_dim < dim, BASELINE configs[3] / [4]): one CTA per (request, KV
+// head) runs the G query heads that share it, so each cached K / V row is staged into shared
+// memory once instead of once per query head (G x fewer CTAs and K/V transfers). Per head the
+// arithmetic and summation order are attn128_kernel's, so the outputs are bit-identical.
+template <int G>
+__global__ void __launch_bounds__(kA2Threads)
+    attn128g_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos_dev, uint16_t* __restrict__ ctx_out,
+                    int ld_ctx, int stage_rows_max) {
+    constexpr int hd = 128, half = 64;
+    extern __shared__ __align__(16) float sm[];
+    float* qs = sm;                  // [G][hd]
+    float* ks = qs + G * hd;         // hd (this step's key, bf16-rounded)
+    float* vs = ks + hd;             // hd
+    uint16_t* st = reinterpret_cast<uint16_t*>(vs + hd);                 // [stage_rows_max][hd]: K, then V, then partials
+    float* scores = reinterpret_cast<float*>(st + stage_rows_max * hd);  // [G][max_seq]
+    __shared__ float red[32];
+    const unsigned long long t_entry = gtimer();
+    if (BD_PDL_EARLY) griddep_launch_dependents();  // next linear's prologue may start
+    const int kh = blockIdx.x, b = blockIdx.y;
+    const int pos = pos_dev[b];
+    const int n_ctx = pos + 1;
+    const int rs = threadIdx.x >> 4, dg = threadIdx.x & 15;
+    uint16_t* kc = a.kcache[b] + (static_cast<size_t>(a.layer) * a.max_seq) * a.kv_dim + kh * hd;
+    uint16_t* vc = a.vcache[b] + (static_cast<size_t>(a.layer) * a.max_seq) * a.kv_dim + kh * hd;
+    stage_rows(st, kc, 0, min(n_ctx, stage_rows_max), a.kv_dim);  // earlier steps' rows: before the wait
+    griddep_wait();  // PDL: q/k/v partials come from the previous kernel
+    const unsigned long long t_wait = gtimer();
+
+    const float2* rope = a.rope + static_cast<size_t>(pos) * half;
+    for (int i = threadIdx.x; i < (G + 2) * hd; i += kA2Threads) {
+        const int which = i / hd, d = i - which * hd;  // < G: query head kh G + which; G: key; G + 1: value
+        const int col = which < G ? (kh * G + which) * hd + d
+                                  : (which == G ? a.dim + kh * hd + d : a.dim + a.kv_dim + kh * hd + d);
+        const float v = proj_val(qkv, b, col);
+        (which < G ? qs + which * hd : (which == G ? ks : vs))[d] = which == G + 1 ? bf16_to_f32(f32_to_bf16(v)) : v;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < (G + 1) * half; i += kA2Threads) {
+        const int which = i / half, pi = i - which * half;
+        float* buf = which < G ? qs + which * hd : ks;
+        const float2 cs = rope[pi];
+        const float v0 = buf[2 * pi], v1 = buf[2 * pi + 1];
+        const float r0 = v0 * cs.x - v1 * cs.y, r1 = v0 * cs.y + v1 * cs.x;
+        if (which < G) {
+            buf[2 * pi] = r0;
+            buf[2 * pi + 1] = r1;
+        } else {
+            buf[2 * pi] = bf16_to_f32(f32_to_bf16(r0));
+            buf[2 * pi + 1] = bf16_to_f32(f32_to_bf16(r1));
+        }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (threadIdx.x < hd) {  // KV append (serve.cpp:261-264), post-RoPE
+        kc[static_cast<size_t>(pos) * a.kv_dim + threadIdx.x] = f32_to_bf16(ks[threadIdx.x]);
+        vc[static_cast<size_t>(pos) * a.kv_dim + threadIdx.x] = f32_to_bf16(vs[threadIdx.x]);
+    }
+    const float inv_sqrt_hd = 1.0f / sqrtf(static_cast<float>(hd));
+    float q[G][8], kn[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) q[g][e] = qs[g * hd + 8 * dg + e];
+        kn[e] = ks[8 * dg + e];
+    }
+    for (int c0 = 0; c0 < n_ctx; c0 += stage_rows_max) {
+        const int nr = min(stage_rows_max, n_ctx - c0);
+        if (c0) {
+            __syncthreads();
+            stage_rows(st, kc, c0, nr, a.kv_dim);
+            cp_async_wait_all();
+            __syncthreads();
+        }
+        for (int rb = 0; rb < nr; rb += 16) {
+            const int r = rb + rs, j = c0 + r;
+            float k8[8];
+            bf16x8_to_f32(r < nr ? *reinterpret_cast<const uint4*>(st + r * hd + 8 * dg) : make_uint4(0u, 0u, 0u, 0u),
+                          k8);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                float acc = 0.0f;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc += q[g][e] * (j == pos ? kn[e] : k8[e]);
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (dg == 0 && r < nr) scores[g * a.max_seq + j] = acc * inv_sqrt_hd;
+            }
+        }
+    }
+    __syncthreads();
+    stage_rows(st, vc, 0, min(n_ctx, stage_rows_max), a.kv_dim);  // streams in during the softmax
+    float sum[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        float* sc = scores + g * a.max_seq;
+        float mx = -INFINITY;
+        for (int j = threadIdx.x; j < n_ctx; j += kA2Threads) mx = fmaxf(mx, sc[j]);
+        mx = block_max(mx, red);
+        float sg = 0.0f;
+        for (int j = threadIdx.x; j < n_ctx; j += kA2Threads) {
+            const float e = expf(sc[j] - mx);
+            sc[j] = e;
+            sg += e;
+        }
+        sum[g] = block_sum(sg, red);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    float acc[G][8];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[g][e] = 0.0f;
+    float vn[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) vn[e] = vs[8 * dg + e];
+    for (int c0 = 0; c0 < n_ctx; c0 += stage_rows_max) {
+        const int nr = min(stage_rows_max, n_ctx - c0);
+        if (c0) {
+            __syncthreads();
+            stage_rows(st, vc, c0, nr, a.kv_dim);
+            cp_async_wait_all();
+            __syncthreads();
+        }
+        for (int r = rs; r < nr; r += 16) {
+            const int j = c0 + r;
+            float v8[8];
+            bf16x8_to_f32(*reinterpret_cast<const uint4*>(st + r * hd + 8 * dg), v8);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const float pj = scores[g * a.max_seq + j] / sum[g];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[g][e] += pj * (j == pos ? vn[e] : v8[e]);
+            }
+        }
+    }
+    float* part = reinterpret_cast<float*>(st);  // [16][hd] f32 row-slot partials, one head at a time
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) part[rs * hd + 8 * dg + e] = acc[g][e];
+        __syncthreads();
+        if (threadIdx.x < hd) {
+            float t = 0.0f;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) t += part[r * hd + threadIdx.x];
+            ctx_out[size_t(b) * ld_ctx + (kh * G + g) * hd + threadIdx.x] = f32_to_bf16(t);
+        }
+    }
+    if (threadIdx.x == 0) trace_rec(TR_ATTN, t_entry, t_wait);
+}
+
 // act = silu(gate) * up (serve.cpp:301-302)
 __global__ void silu_kernel(ProjOut gu, int inter, uint16_t* __restrict__ act, int ld_act) {
     const int b = blockIdx.y;
@@ -796,6 +949,28 @@ void resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const 
 
 void attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int batch,
                  uint16_t* ctx, int ld_ctx, cudaStream_t s) {
+    const int group = a.n_heads / a.n_kv_heads;
+    if (a.hd == 128 && a.kv_dim % 8 == 0 && a.dim % 8 == 0 && (group == 2 || group == 4 || group == 8)) {
+        // grouped-query heads: one CTA per (request, KV head), K / V staged once for the group
+        const int rows = std::min(192, std::max(32, a.max_seq));
+        const size_t smem = ((group + 2) * 128 + size_t(group) * a.max_seq) * sizeof(float) + size_t(rows) * 128 * 2;
+        require(smem <= 220 * 1024, BD_ERR_BAD_ARGUMENT, "attention: max_seq too large for the score buffer");
+        static bool attr[3] = {false, false, false};
+        auto launch = [&](auto kern, int gi) {
+            if (!attr[gi]) {
+                BD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+                attr[gi] = true;
+            }
+            BD_CUDA(launch_pdl(kern, dim3(a.n_kv_heads, batch), dim3(kA2Threads), smem, s, qkv, a, pos_dev, ctx, ld_ctx,
+                               rows));
+        };
+        if (group == 2) launch(attn128g_kernel<2>, 0);
+        else if (group == 4) launch(attn128g_kernel<4>, 1);
+        else launch(attn128g_kernel<8>, 2);
+        note_launch();
+        BD_CUDA(cudaGetLastError());
+        return;
+    }
     if (a.hd == 128 && a.kv_dim % 8 == 0 && a.dim % 8 == 0) {
         // one staging buffer of up to 192 rows (48 KB: K, then V): four CTAs per SM,
         // so batch x heads = 512 CTAs run as a single wave on 148 SMs
