@@ -653,8 +653,10 @@ __global__ void __launch_bounds__(kA2Threads)
 // head) runs the G query heads that share it, so each cached K / V row is staged into shared
 // memory once instead of once per query head (G x fewer CTAs and K/V transfers). Per head the
 // arithmetic and summation order are attn128_kernel's, so the outputs are bit-identical.
+// G <= 4: <= 64 registers, so 4 CTAs share an SM and batch 64 x 8 KV heads = 512 CTAs run as
+// one wave on 148 SMs (at 80 registers the last 68 CTAs formed a second wave: +15 us per layer)
 template <int G>
-__global__ void __launch_bounds__(kA2Threads)
+__global__ void __launch_bounds__(kA2Threads, G <= 4 ? 4 : 2)
     attn128g_kernel(ProjOut qkv, AttnArgs a, const int* __restrict__ pos_dev, uint16_t* __restrict__ ctx_out,
                     int ld_ctx, int stage_rows_max) {
     constexpr int hd = 128, half = 64;

@@ -45,10 +45,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="l7_stack")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "timeline.txt"))
+    ap.add_argument("--tenants", type=int, default=0)
     args = ap.parse_args()
     wl = bench.WORKLOADS[args.workload]
     arch = dict(wl["arch"], rope_theta=10000.0)
-    T, B, ctx = wl["tenants"], wl["batch"], wl["ctx"]
+    T, B, ctx = args.tenants or wl["tenants"], wl["batch"], wl["ctx"]
     arch["max_seq"] = ctx + 16
     dev = torch.device("cuda:0")
     pool, _, _ = bench.build_pool(arch, T, dev, seed=1234)
