@@ -649,6 +649,30 @@ __global__ void __launch_bounds__(kA2Threads)
     if (threadIdx.x == 0) trace_rec(TR_ATTN, t_entry, t_wait);
 }
 
+// block_max (kMax) / block_sum of G values at once, each in their order
+template <int G, bool kMax>
+__device__ __forceinline__ void block_reduce_g(float (&v)[G], float* red) {
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float w = __shfl_xor_sync(0xffffffffu, v[g], o);
+            v[g] = kMax ? fmaxf(v[g], w) : v[g] + w;
+        }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (l == 0)
+#pragma unroll
+        for (int g = 0; g < G; ++g) red[g * 32 + w] = v[g];
+    __syncthreads();
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        float t = kMax ? red[g * 32] : 0.0f;
+        for (int i = kMax ? 1 : 0; i < nw; ++i) t = kMax ? fmaxf(t, red[g * 32 + i]) : t + red[g * 32 + i];
+        v[g] = t;
+    }
+}
+
 // Grouped-query attention (kv_dim < dim, BASELINE configs[3] / [4]): one CTA per (request, KV
 // head) runs the G query heads that share it, so each cached K / V row is staged into shared
 // memory once instead of once per query head (G x fewer CTAs and K/V transfers). Per head the
@@ -666,7 +690,7 @@ __global__ void __launch_bounds__(kA2Threads, G <= 4 ? 4 : 2)
     float* vs = ks + hd;             // hd
     uint16_t* st = reinterpret_cast<uint16_t*>(vs + hd);                 // [stage_rows_max][hd]: K, then V, then partials
     float* scores = reinterpret_cast<float*>(st + stage_rows_max * hd);  // [G][max_seq]
-    __shared__ float red[32];
+    __shared__ float redg[G * 32];
     const unsigned long long t_entry = gtimer();
     if (BD_PDL_EARLY) griddep_launch_dependents();  // next linear's prologue may start
     const int kh = blockIdx.x, b = blockIdx.y;
@@ -742,21 +766,26 @@ __global__ void __launch_bounds__(kA2Threads, G <= 4 ? 4 : 2)
     }
     __syncthreads();
     stage_rows(st, vc, 0, min(n_ctx, stage_rows_max), a.kv_dim);  // streams in during the softmax
-    float sum[G];
+    // softmax of the G heads with one pair of block reductions (per head the order of
+    // block_max / block_sum)
+    float mx[G], sum[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        mx[g] = -INFINITY;
+        for (int j = threadIdx.x; j < n_ctx; j += kA2Threads) mx[g] = fmaxf(mx[g], scores[g * a.max_seq + j]);
+    }
+    block_reduce_g<G, true>(mx, redg);
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         float* sc = scores + g * a.max_seq;
-        float mx = -INFINITY;
-        for (int j = threadIdx.x; j < n_ctx; j += kA2Threads) mx = fmaxf(mx, sc[j]);
-        mx = block_max(mx, red);
-        float sg = 0.0f;
+        sum[g] = 0.0f;
         for (int j = threadIdx.x; j < n_ctx; j += kA2Threads) {
-            const float e = expf(sc[j] - mx);
+            const float e = expf(sc[j] - mx[g]);
             sc[j] = e;
-            sg += e;
+            sum[g] += e;
         }
-        sum[g] = block_sum(sg, red);
     }
+    block_reduce_g<G, false>(sum, redg);
     cp_async_wait_all();
     __syncthreads();
     float acc[G][8];
@@ -787,18 +816,34 @@ __global__ void __launch_bounds__(kA2Threads, G <= 4 ? 4 : 2)
             }
         }
     }
-    float* part = reinterpret_cast<float*>(st);  // [16][hd] f32 row-slot partials, one head at a time
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
+    float* part = reinterpret_cast<float*>(st);  // f32 row-slot partials [heads][16][hd]
+    if (stage_rows_max * hd * 2 >= G * 16 * hd * 4) {  // all G heads in one pass
         __syncthreads();
 #pragma unroll
-        for (int e = 0; e < 8; ++e) part[rs * hd + 8 * dg + e] = acc[g][e];
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) part[(g * 16 + rs) * hd + 8 * dg + e] = acc[g][e];
         __syncthreads();
-        if (threadIdx.x < hd) {
+        for (int i = threadIdx.x; i < G * hd; i += kA2Threads) {
+            const int g = i / hd, d = i - g * hd;
             float t = 0.0f;
 #pragma unroll
-            for (int r = 0; r < 16; ++r) t += part[r * hd + threadIdx.x];
-            ctx_out[size_t(b) * ld_ctx + (kh * G + g) * hd + threadIdx.x] = f32_to_bf16(t);
+            for (int r = 0; r < 16; ++r) t += part[(g * 16 + r) * hd + d];
+            ctx_out[size_t(b) * ld_ctx + (kh * G + g) * hd + d] = f32_to_bf16(t);
+        }
+    } else {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            __syncthreads();
+#pragma unroll
+            for (int e = 0; e < 8; ++e) part[rs * hd + 8 * dg + e] = acc[g][e];
+            __syncthreads();
+            if (threadIdx.x < hd) {
+                float t = 0.0f;
+#pragma unroll
+                for (int r = 0; r < 16; ++r) t += part[r * hd + threadIdx.x];
+                ctx_out[size_t(b) * ld_ctx + (kh * G + g) * hd + threadIdx.x] = f32_to_bf16(t);
+            }
         }
     }
     if (threadIdx.x == 0) trace_rec(TR_ATTN, t_entry, t_wait);
