@@ -611,6 +611,8 @@ __global__ void __launch_bounds__(kA2Threads)
         sum += e;
     }
     sum = block_sum(sum, red);
+    // p_j = e_j / sum once per row (not once per row and dims group in the PV loop)
+    for (int j = threadIdx.x; j < n_ctx; j += kA2Threads) scores[j] = scores[j] / sum;
     cp_async_wait_all();
     __syncthreads();
     // ctx (serve.cpp:276-281): p_j = e_j / sum; row-slot partials added in slot order
@@ -628,7 +630,7 @@ __global__ void __launch_bounds__(kA2Threads)
         }
         for (int r = rs; r < nr; r += 16) {
             const int j = c0 + r;
-            const float pj = scores[j] / sum;
+            const float pj = scores[j];
             float v8[8];
             bf16x8_to_f32(*reinterpret_cast<const uint4*>(st + r * hd + 8 * dg), v8);
 #pragma unroll
@@ -754,10 +756,14 @@ __global__ void __launch_bounds__(kA2Threads, G <= 4 ? 4 : 2)
             bf16x8_to_f32(r < nr ? *reinterpret_cast<const uint4*>(st + r * hd + 8 * dg) : make_uint4(0u, 0u, 0u, 0u),
                           k8);
 #pragma unroll
+            if (j == pos)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) k8[e] = kn[e];
+#pragma unroll
             for (int g = 0; g < G; ++g) {
                 float acc = 0.0f;
 #pragma unroll
-                for (int e = 0; e < 8; ++e) acc += q[g][e] * (j == pos ? kn[e] : k8[e]);
+                for (int e = 0; e < 8; ++e) acc += q[g][e] * k8[e];
 #pragma unroll
                 for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
                 if (dg == 0 && r < nr) scores[g * a.max_seq + j] = acc * inv_sqrt_hd;
@@ -786,6 +792,10 @@ __global__ void __launch_bounds__(kA2Threads, G <= 4 ? 4 : 2)
         }
     }
     block_reduce_g<G, false>(sum, redg);
+    // p_j = e_j / sum once per row and head (not in the PV loop)
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+        for (int j = threadIdx.x; j < n_ctx; j += kA2Threads) scores[g * a.max_seq + j] = scores[g * a.max_seq + j] / sum[g];
     cp_async_wait_all();
     __syncthreads();
     float acc[G][8];
@@ -810,7 +820,7 @@ __global__ void __launch_bounds__(kA2Threads, G <= 4 ? 4 : 2)
             bf16x8_to_f32(*reinterpret_cast<const uint4*>(st + r * hd + 8 * dg), v8);
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-                const float pj = scores[g * a.max_seq + j] / sum[g];
+                const float pj = scores[g * a.max_seq + j];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) acc[g][e] += pj * (j == pos ? vn[e] : v8[e]);
             }
