@@ -59,6 +59,18 @@ __device__ __forceinline__ uint16_t f32_to_bf16(float v) {
     return __bfloat16_as_ushort(__float2bfloat16_rn(v));
 }
 
+// K3d gathered copy (XgOut): column c of request b
+__device__ __forceinline__ void xg_store(const XgOut& xo, int b, int c, uint16_t v) {
+    const int j = c & 31;
+    xo.xg[static_cast<size_t>(xo.row[b]) * xo.ld + (c & ~31) + (j < 16 ? 2 * j : 2 * (j - 16) + 1)] = v;
+}
+__device__ __forceinline__ void xg_store4(const XgOut& xo, int b, int c, uint2 pk) {
+    xg_store(xo, b, c, uint16_t(pk.x & 0xFFFFu));
+    xg_store(xo, b, c + 1, uint16_t(pk.x >> 16));
+    xg_store(xo, b, c + 2, uint16_t(pk.y & 0xFFFFu));
+    xg_store(xo, b, c + 3, uint16_t(pk.y >> 16));
+}
+
 template <typename T>
 __device__ T block_sum(T v, T* red) {
 #pragma unroll
@@ -182,7 +194,7 @@ __device__ __forceinline__ void proj_val4_pair(const ProjOut& p, int b, int m, i
 __global__ void __launch_bounds__(kRnThreads)
     resid_norm_kernel(float* __restrict__ x, int dim, ProjOut proj, const float* const* __restrict__ norm_w,
                       uint16_t* __restrict__ xn, int ldxn, float* __restrict__ xn_f32,
-                      unsigned* __restrict__ arrive, double* __restrict__ msq_part) {
+                      unsigned* __restrict__ arrive, double* __restrict__ msq_part, XgOut xo) {
     __shared__ double red_d[32];
     __shared__ double inv_s;
     const unsigned long long t_entry = gtimer();
@@ -230,6 +242,7 @@ __global__ void __launch_bounds__(kRnThreads)
         pk.x = uint32_t(f32_to_bf16(y0)) | (uint32_t(f32_to_bf16(y1)) << 16);
         pk.y = uint32_t(f32_to_bf16(y2)) | (uint32_t(f32_to_bf16(y3)) << 16);
         *reinterpret_cast<uint2*>(xn + size_t(b) * ldxn + i) = pk;
+        if (xo.xg) xg_store4(xo, b, i, pk);
     }
     if (xn_f32) *reinterpret_cast<float4*>(xn_f32 + size_t(b) * dim + i) = make_float4(y0, y1, y2, y3);
     if (threadIdx.x == 0) trace_rec(TR_NORM, t_entry, t_wait);
@@ -240,7 +253,7 @@ __global__ void __launch_bounds__(kRnThreads)
 // a global arrival counter (same addition order -> same bits).
 __global__ void __launch_bounds__(kRnThreads)
     resid_norm_cluster_kernel(float* __restrict__ x, int dim, ProjOut proj, const float* const* __restrict__ norm_w,
-                              uint16_t* __restrict__ xn, int ldxn, float* __restrict__ xn_f32) {
+                              uint16_t* __restrict__ xn, int ldxn, float* __restrict__ xn_f32, XgOut xo) {
     __shared__ double red_d[32];
     __shared__ double part_sq;
     __shared__ double inv_s;
@@ -293,6 +306,7 @@ __global__ void __launch_bounds__(kRnThreads)
         pk.x = uint32_t(f32_to_bf16(y0)) | (uint32_t(f32_to_bf16(y1)) << 16);
         pk.y = uint32_t(f32_to_bf16(y2)) | (uint32_t(f32_to_bf16(y3)) << 16);
         *reinterpret_cast<uint2*>(xn + size_t(b) * ldxn + i) = pk;
+        if (xo.xg) xg_store4(xo, b, i, pk);
     }
     if (xn_f32) *reinterpret_cast<float4*>(xn_f32 + size_t(b) * dim + i) = make_float4(y0, y1, y2, y3);
     if (threadIdx.x == 0) trace_rec(TR_NORM, t_entry, t_wait);
@@ -646,7 +660,9 @@ __global__ void __launch_bounds__(kA2Threads)
         float t = 0.0f;
 #pragma unroll
         for (int r = 0; r < 16; ++r) t += part[r * hd + threadIdx.x];
-        ctx_out[size_t(b) * ld_ctx + h * hd + threadIdx.x] = f32_to_bf16(t);
+        const uint16_t v = f32_to_bf16(t);
+        ctx_out[size_t(b) * ld_ctx + h * hd + threadIdx.x] = v;
+        if (a.xo.xg) xg_store(a.xo, b, h * hd + threadIdx.x, v);
     }
     if (threadIdx.x == 0) trace_rec(TR_ATTN, t_entry, t_wait);
 }
@@ -839,7 +855,9 @@ __global__ void __launch_bounds__(kA2Threads, G <= 4 ? 4 : 2)
             float t = 0.0f;
 #pragma unroll
             for (int r = 0; r < 16; ++r) t += part[(g * 16 + r) * hd + d];
-            ctx_out[size_t(b) * ld_ctx + (kh * G + g) * hd + d] = f32_to_bf16(t);
+            const uint16_t v = f32_to_bf16(t);
+            ctx_out[size_t(b) * ld_ctx + (kh * G + g) * hd + d] = v;
+            if (a.xo.xg) xg_store(a.xo, b, (kh * G + g) * hd + d, v);
         }
     } else {
 #pragma unroll
@@ -852,7 +870,9 @@ __global__ void __launch_bounds__(kA2Threads, G <= 4 ? 4 : 2)
                 float t = 0.0f;
 #pragma unroll
                 for (int r = 0; r < 16; ++r) t += part[r * hd + threadIdx.x];
-                ctx_out[size_t(b) * ld_ctx + (kh * G + g) * hd + threadIdx.x] = f32_to_bf16(t);
+                const uint16_t v = f32_to_bf16(t);
+                ctx_out[size_t(b) * ld_ctx + (kh * G + g) * hd + threadIdx.x] = v;
+                if (a.xo.xg) xg_store(a.xo, b, (kh * G + g) * hd + threadIdx.x, v);
             }
         }
     }
@@ -870,7 +890,7 @@ __global__ void silu_kernel(ProjOut gu, int inter, uint16_t* __restrict__ act, i
     }
 }
 // 4 outputs per thread (aligned shapes), same per-element arithmetic
-__global__ void silu4_kernel(ProjOut gu, int inter, uint16_t* __restrict__ act, int ld_act) {
+__global__ void silu4_kernel(ProjOut gu, int inter, uint16_t* __restrict__ act, int ld_act, XgOut xo) {
     const unsigned long long t_entry = gtimer();
     if (BD_PDL_EARLY) griddep_launch_dependents();  // next linear's prologue may start
     griddep_wait();  // PDL: gate/up partials come from the previous kernel
@@ -884,6 +904,7 @@ __global__ void silu4_kernel(ProjOut gu, int inter, uint16_t* __restrict__ act, 
         pk.x = uint32_t(f(g.x, u.x)) | (uint32_t(f(g.y, u.y)) << 16);
         pk.y = uint32_t(f(g.z, u.z)) | (uint32_t(f(g.w, u.w)) << 16);
         *reinterpret_cast<uint2*>(act + size_t(b) * ld_act + i) = pk;
+        if (xo.xg) xg_store4(xo, b, i, pk);
     }
     if (threadIdx.x == 0) trace_rec(TR_SILU, t_entry, t_wait);
 }
@@ -970,8 +991,8 @@ size_t norm_ws_bytes(int batch, int dim) {
     return cnt + size_t(batch) * std::max(norm_chunks(dim), (dim + kRnChunk - 1) / kRnChunk) * sizeof(double);
 }
 
-void resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const float* const* norm_w,
-                       uint16_t* xn, int ldxn, float* xn_f32, void* ws, cudaStream_t s) {
+bool resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const float* const* norm_w,
+                       uint16_t* xn, int ldxn, float* xn_f32, void* ws, cudaStream_t s, const XgOut& xo) {
     unsigned* arrive = static_cast<unsigned*>(ws);
     double* msq_ws = reinterpret_cast<double*>(static_cast<char*>(ws) +
                                                (size_t(batch) * sizeof(unsigned) + 255) / 256 * 256);
@@ -980,31 +1001,32 @@ void resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const 
     const int nc = (dim + kRnChunk - 1) / kRnChunk;
     if (norm_w && dim % 4 == 0 && ldxn % 4 == 0 && proj_vec4_ok(proj) && nc >= 2 && nc <= 8) {
         BD_CUDA(launch_pdl_cluster(resid_norm_cluster_kernel, dim3(nc, batch), dim3(kRnThreads), 0, s, unsigned(nc),
-                                   x, dim, proj, norm_w, xn, ldxn, xn_f32));
+                                   x, dim, proj, norm_w, xn, ldxn, xn_f32, xo));
         note_launch();
         BD_CUDA(cudaGetLastError());
-        return;
+        return xo.xg != nullptr;
     }
     if (dim % 4 == 0 && ldxn % 4 == 0 && proj_vec4_ok(proj) &&
         size_t(nc) * batch <= size_t(kNumSMs) * 8) {
         BD_CUDA(launch_pdl(resid_norm_kernel, dim3(nc, batch), dim3(kRnThreads), 0, s, x, dim, proj, norm_w, xn,
-                           ldxn, xn_f32, arrive, msq_ws));
+                           ldxn, xn_f32, arrive, msq_ws, xo));
         note_launch();
         BD_CUDA(cudaGetLastError());
-        return;
+        return xo.xg != nullptr;
     }
     // two-phase fallback (unaligned shapes / grids too wide to be co-resident)
     const dim3 grid(norm_chunks(dim), batch);
     resid_kernel<<<grid, kNormChunk, 0, s>>>(x, dim, proj, norm_w ? msq_ws : nullptr);
     note_launch();
     BD_CUDA(cudaGetLastError());
-    if (!norm_w) return;
+    if (!norm_w) return false;
     norm_kernel<<<grid, kNormChunk, 0, s>>>(x, dim, msq_ws, norm_w, xn, ldxn, xn_f32);
     note_launch();
     BD_CUDA(cudaGetLastError());
+    return false;
 }
 
-void attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int batch,
+bool attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int batch,
                  uint16_t* ctx, int ld_ctx, cudaStream_t s) {
     const int group = a.n_heads / a.n_kv_heads;
     if (a.hd == 128 && a.kv_dim % 8 == 0 && a.dim % 8 == 0 && (group == 2 || group == 4 || group == 8)) {
@@ -1026,7 +1048,7 @@ void attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int 
         else launch(attn128g_kernel<8>, 2);
         note_launch();
         BD_CUDA(cudaGetLastError());
-        return;
+        return a.xo.xg != nullptr;
     }
     if (a.hd == 128 && a.kv_dim % 8 == 0 && a.dim % 8 == 0) {
         // one staging buffer of up to 192 rows (48 KB: K, then V): four CTAs per SM,
@@ -1043,7 +1065,7 @@ void attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int 
                            ld_ctx, rows));
         note_launch();
         BD_CUDA(cudaGetLastError());
-        return;
+        return a.xo.xg != nullptr;
     }
     constexpr int kAttnThreads = 256;
     const size_t smem = (3 * a.hd + a.max_seq + (kAttnThreads / 32) * a.hd) * sizeof(float);
@@ -1055,18 +1077,21 @@ void attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int 
     attn_kernel<<<dim3(a.n_heads, batch), kAttnThreads, smem, s>>>(qkv, a, pos_dev, ctx, ld_ctx);
     note_launch();
     BD_CUDA(cudaGetLastError());
+    return false;
 }
 
-void silu_launch(const ProjOut& gu, int batch, int inter, uint16_t* act, int ld_act, cudaStream_t s) {
+bool silu_launch(const ProjOut& gu, int batch, int inter, uint16_t* act, int ld_act, cudaStream_t s,
+                 const XgOut& xo) {
     if (inter % 4 == 0 && ld_act % 4 == 0 && proj_vec4_ok(gu)) {
         const int bx = std::max(1, std::min((inter / 4 + 127) / 128, 64));
-        BD_CUDA(launch_pdl(silu4_kernel, dim3(bx, batch), dim3(128), 0, s, gu, inter, act, ld_act));
+        BD_CUDA(launch_pdl(silu4_kernel, dim3(bx, batch), dim3(128), 0, s, gu, inter, act, ld_act, xo));
     } else {
         const int bx = std::max(1, std::min((inter + 255) / 256, 64));
         silu_kernel<<<dim3(bx, batch), 256, 0, s>>>(gu, inter, act, ld_act);
     }
     note_launch();
     BD_CUDA(cudaGetLastError());
+    return xo.xg != nullptr && inter % 4 == 0 && ld_act % 4 == 0 && proj_vec4_ok(gu);
 }
 
 void embed_launch(const float* embed, const int* tokens, const float* const* embed_delta, int batch,

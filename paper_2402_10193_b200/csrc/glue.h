@@ -28,22 +28,35 @@ void shard_reduce_launch(const ProjOut& p, int batch, int n_l, float* dst, cudaS
 void gather_transpose_launch(const uint16_t* src, int world, int batch, int n_l, uint16_t* dst, int ld,
                              cudaStream_t s);
 
+// K3d's gathered activations written directly by the kernel producing a projection's input
+// (instead of mtd_gather_kernel): request b's row goes to row[b] of xg, each 32-column block in
+// the MMA's column order (2 i <- i, 2 i + 1 <- i + 16); padding rows stay zero
+struct XgOut {
+    uint16_t* xg = nullptr;
+    int ld = 0;
+    const int* row = nullptr;  // [batch]
+};
+
 struct AttnArgs {
     int dim, kv_dim, n_heads, n_kv_heads, hd, max_seq, layer;
     uint16_t* const* kcache;  // per request: [n_layers][max_seq][kv_dim] bf16
     uint16_t* const* vcache;
     const float2* rope;       // [max_seq][hd/2] (cos, sin)
+    XgOut xo{};               // optional K3d copy of ctx (hd 128 kernels)
 };
 
 // ws: norm_ws_bytes(batch, dim) bytes, zeroed once at allocation (arrival counters
 // + chunk sums of squares); launches using one ws must be stream-ordered
 int norm_chunks(int dim);
 size_t norm_ws_bytes(int batch, int dim);
-void resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const float* const* norm_w,
-                       uint16_t* xn, int ldxn, float* xn_f32, void* ws, cudaStream_t s);
-void attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int batch,
+// the launchers write an XgOut copy on their one-launch / head_dim-128 paths and return whether
+// they did (false: the caller gathers)
+bool resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const float* const* norm_w,
+                       uint16_t* xn, int ldxn, float* xn_f32, void* ws, cudaStream_t s, const XgOut& xo = XgOut{});
+bool attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int batch,
                  uint16_t* ctx, int ld_ctx, cudaStream_t s);
-void silu_launch(const ProjOut& gu, int batch, int inter, uint16_t* act, int ld_act, cudaStream_t s);
+bool silu_launch(const ProjOut& gu, int batch, int inter, uint16_t* act, int ld_act, cudaStream_t s,
+                 const XgOut& xo = XgOut{});
 void embed_launch(const float* embed, const int* tokens, const float* const* embed_delta, int batch,
                   int dim, float* x, cudaStream_t s);
 void logits_launch(const ProjOut& lm, const float* const* raw_delta, const float* xn_f32, int batch,

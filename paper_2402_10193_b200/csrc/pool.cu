@@ -194,6 +194,10 @@ struct Plan {
     std::vector<std::array<Md, 4>> mtd;
     uint16_t* xg = nullptr;  // gathered activations (tenant-major, padded), K3d only
     int xg_ld = 0;
+    // every K3d group gathers the same way: the glue kernel producing a K3d group's input writes
+    // its gathered copy (XgOut, row d_xrow[b] for request b) and the gather launch is skipped
+    bool xg_direct = false;
+    int* d_xrow = nullptr;
     uint8_t* xpk = nullptr;  // FP4 activation pieces + scales [B][chunks][kXpBlock]
     cudaGraphExec_t graph_layers = nullptr, graph_full = nullptr;
     uint64_t kernels_layers = 0, kernels_full = 0;
@@ -252,6 +256,7 @@ struct PoolImpl {
     // auto | lut | mt4 | units; BD_DELTA forces one K3 variant (test hook: every variant is
     // checked against the oracle on the same inputs)
     std::string delta_mode = "auto";
+    bool xg_done = false;  // the next K3d linear's gathered input was written by its producer
 
     ~PoolImpl() {
         cudaSetDevice(device);
@@ -950,6 +955,36 @@ struct PoolImpl {
             if (!ok)
                 for (uint64_t l = 0; l < nL; ++l) p.mtd[l][gi].ok = false;
         }
+        // one gather map for every K3d group (the same tenant / request lists): the producers
+        // of their inputs write the gathered rows themselves (XgOut)
+        const MtdGather* g0 = nullptr;
+        bool same = world == 1;
+        for (uint64_t l = 0; l < nL; ++l)
+            for (int gi = 0; gi < 4; ++gi)
+                if (p.mtd[l][gi].ok) {
+                    if (!g0) g0 = &p.mtd[l][gi].gat;
+                    else same = same && std::memcmp(g0, &p.mtd[l][gi].gat, sizeof(MtdGather)) == 0;
+                }
+        if (g0 && same) {
+            std::vector<int> row(p.B, -1);
+            for (int t = 0; t < kMtdMaxTenants; ++t)
+                for (int i = 0; i < g0->n_req[t]; ++i) row[g0->req[t][i]] = g0->row0[t] + i;
+            if (std::find(row.begin(), row.end(), -1) == row.end()) {
+                p.d_xrow = dmalloc<int>(row.size(), &p.allocs);
+                BD_CUDA(cudaMemcpy(p.d_xrow, row.data(), row.size() * sizeof(int), cudaMemcpyHostToDevice));
+                p.xg_direct = true;
+            }
+        }
+    }
+    // XgOut for the input of group gi of layer l (empty unless that group runs K3d)
+    XgOut xg_out(const Plan& p, uint64_t l, int gi) const {
+        XgOut o;
+        if (p.xg_direct && mtd_ok(p, l, gi)) {
+            o.xg = p.xg;
+            o.ld = p.xg_ld;
+            o.row = p.d_xrow;
+        }
+        return o;
     }
 
     // K23 (mt4.cu): base GEMM + every tenant plane as FP4 MMAs in one persistent
@@ -1357,7 +1392,9 @@ struct PoolImpl {
         if (mtd_ok(p, l, group)) {
             // K2 and K3d both hold the SM's tensor memory: one after the other
             const Plan::Md& md = p.mtd[l][group];
-            prof(BD_PROF_XQ_PREP, s, [&] { mtd_gather_launch(X, ldx, cols, md.gat, md.prm.n_ten, p.xg, p.xg_ld, s); });
+            if (!xg_done)
+                prof(BD_PROF_XQ_PREP, s, [&] { mtd_gather_launch(X, ldx, cols, md.gat, md.prm.n_ten, p.xg, p.xg_ld, s); });
+            xg_done = false;
             prof(BD_PROF_GEMM_QKV + group, s, [&] { base_gemm(g, l, group, mw, mx, s); });
             prof(BD_PROF_DELTA_QKV + group, s, [&] { mtd_launch(md.prm, s); });
             return;
@@ -1467,16 +1504,17 @@ struct PoolImpl {
             const LayerW& W = L[l];
             // x += down(prev); xn = norm1(x)   (x and xn replicated on every rank)
             prof(BD_PROF_NORM, s, [&] {
-                resid_norm_launch(x, B, int(a.dim), prev, p.d_norm + (2 * l) * B, xn, int(ld_dim),
-                                  nullptr, msq, s);
+                xg_done = resid_norm_launch(x, B, int(a.dim), prev, p.d_norm + (2 * l) * B, xn, int(ld_dim),
+                                            nullptr, msq, s, xg_out(p, l, 0));
             });
             const bool i8 = base_kind == 2;
             linear(p, l, 0, p.g_qkv, i8 ? W.m8[0] : W.m_qkv, i8 ? p.xq_dim : p.x_xn, p.units[l][0], xn,
                    int(ld_dim), int(a.dim), B, s);
             aa.layer = int(l);
+            aa.xo = xg_out(p, l, 1);
             prof(BD_PROF_ATTN, s, [&] {
-                attn_launch(group_out(p, l, 0, p.g_qkv), aa, p.d_pos, B, tp ? ctx_loc : ctx,
-                            tp ? int(q_l) : int(ld_dim), s);
+                xg_done = attn_launch(group_out(p, l, 0, p.g_qkv), aa, p.d_pos, B, tp ? ctx_loc : ctx,
+                                      tp ? int(q_l) : int(ld_dim), s);
             });
             if (tp) exchange_bf16(ctx_loc, B, int(q_l), ctx, int(ld_dim), s);
             linear(p, l, 1, p.g_o, i8 ? W.m8[1] : W.m_o, i8 ? p.xq_dim : p.x_ctx, p.units[l][1], ctx,
@@ -1484,14 +1522,14 @@ struct PoolImpl {
             const ProjOut o_out = tp ? exchange_f32(group_out(p, l, 1, p.g_o), B, int(dim_l), s)
                                      : group_out(p, l, 1, p.g_o);
             prof(BD_PROF_NORM, s, [&] {
-                resid_norm_launch(x, B, int(a.dim), o_out, p.d_norm + (2 * l + 1) * B, xn, int(ld_dim),
-                                  nullptr, msq, s);
+                xg_done = resid_norm_launch(x, B, int(a.dim), o_out, p.d_norm + (2 * l + 1) * B, xn, int(ld_dim),
+                                            nullptr, msq, s, xg_out(p, l, 2));
             });
             linear(p, l, 2, p.g_gu, i8 ? W.m8[2] : W.m_gu, i8 ? p.xq_dim : p.x_xn, p.units[l][2], xn,
                    int(ld_dim), int(a.dim), B, s);
             prof(BD_PROF_SILU, s, [&] {
-                silu_launch(group_out(p, l, 2, p.g_gu), B, int(inter_l), tp ? act_loc : act,
-                            tp ? int(inter_l) : int(ld_inter), s);
+                xg_done = silu_launch(group_out(p, l, 2, p.g_gu), B, int(inter_l), tp ? act_loc : act,
+                                      tp ? int(inter_l) : int(ld_inter), s, xg_out(p, l, 3));
             });
             if (tp) exchange_bf16(act_loc, B, int(inter_l), act, int(ld_inter), s);
             linear(p, l, 3, p.g_down, i8 ? W.m8[3] : W.m_down, i8 ? p.xq_inter : p.x_act, p.units[l][3], act,
