@@ -61,8 +61,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     base_gemm_kernel(const __grid_constant__ CUtensorMap map_w,
                      const __grid_constant__ CUtensorMap map_x, float* __restrict__ partial,
                      int M, int N_valid, int bn, int kb_total, int kb_per_split, int splits, int n_units,
-                     int stages, const float* __restrict__ row_scale, const float* __restrict__ piece_scale,
-                     int no_wait) {
+                     int stages, const float* __restrict__ row_scale, const float* __restrict__ piece_scale) {
     extern __shared__ uint8_t smem_raw[];
     const unsigned long long t_entry = gtimer();
     unsigned long long t_wait = 0;
@@ -124,7 +123,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             mbar_arrive_expect_tx(&full[i], L.stage_bytes);
             tma_load_2d_hint(smem + i * L.stage_bytes, &map_w, &full[i], (kb0 + i) * kbk, m0, pol_w);
         }
-        if (!no_wait) griddep_wait();  // PDL: the activations come from the previous kernel
+        griddep_wait();  // PDL: the activations come from the previous kernel
         t_wait = gtimer();
         int it = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
@@ -346,7 +345,7 @@ static void gemm_launch_t(const GemmPlan& p, const CUtensorMap& map_w, const CUt
     const int n_units = p.m_tiles * p.splits;
     BD_CUDA(launch_pdl(base_gemm_kernel<kI8>, dim3(std::min(n_units, p.grid)), dim3(kGemmThreads), size_t(p.smem),
                        stream, map_w, map_x, partial, int(p.M), p.batch, p.bn, p.kb_total, p.kb_per_split, p.splits,
-                       n_units, p.stages, row_scale, piece_scale, p.after_k3d ? 1 : 0));
+                       n_units, p.stages, row_scale, piece_scale));
     note_launch();
     BD_CUDA(cudaGetLastError());
 }

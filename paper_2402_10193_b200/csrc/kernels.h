@@ -18,9 +18,6 @@ struct GemmPlan {
     int batch = 0, bn = 16, stages = 4, smem = 0;
     int m_tiles = 0, kb_total = 0, kb_per_split = 0, splits = 1;
     int grid = 1;  // persistent CTAs (resident slots); units = m_tiles x splits
-    // launched as the programmatic dependent of a K3d grid that has itself waited for X (it
-    // triggers after its griddepcontrol.wait): no wait here, so K2 streams beside K3d
-    bool after_k3d = false;
     bool i8 = false;  // INT8 RTN backbone (kind::i8 against kPieces int8 pieces of X)
 };
 // int8 pieces per activation row (quant_pieces_launch): x = sum_p piece_scale_p * q_p with

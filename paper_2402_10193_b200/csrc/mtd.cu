@@ -131,9 +131,6 @@ __global__ void __launch_bounds__(kThreads, 1) mtd_kernel(const __grid_constant_
         const uint64_t pol_stream = policy_evict_first();
         const uint64_t pol_keep = policy_evict_last();
         griddep_wait();  // PDL: X (gathered by the previous kernel)
-        // X is complete: a K2 launched as this grid's programmatic dependent (side by side on
-        // the SMs this grid leaves free, GemmPlan::after_k3d) may start
-        if (prod == 0 && lane == 0) griddep_launch_dependents();
         int s = 0, gidx = 0;
         uint32_t ph = 0;
         for (int t = t0; t < t1; ++t) {

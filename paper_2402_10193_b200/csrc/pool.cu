@@ -257,7 +257,6 @@ struct PoolImpl {
     // checked against the oracle on the same inputs)
     std::string delta_mode = "auto";
     bool xg_done = false;  // the next K3d linear's gathered input was written by its producer
-    int k3d_sms = 74;      // SMs for K3d beside K2 (0: K2, then K3d on every SM)
 
     ~PoolImpl() {
         cudaSetDevice(device);
@@ -331,7 +330,6 @@ struct PoolImpl {
         BD_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         BD_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
         if (const char* e = std::getenv("BD_DELTA")) delta_mode = e;
-        if (const char* e = std::getenv("BD_K3D_SMS")) k3d_sms = std::atoi(e);  // A/B hook
 
         ld8_dim = round_up(a.dim, 16);
         ld8_inter = round_up(a.intermediate, 16);
@@ -1392,31 +1390,8 @@ struct PoolImpl {
             return;
         }
         if (mtd_ok(p, l, group)) {
+            // K2 and K3d both hold the SM's tensor memory: one after the other
             const Plan::Md& md = p.mtd[l][group];
-            if (concurrent_k23 && k3d_sms > 0 && k3d_sms < kNumSMs) {
-                // K2 and K3d each need a whole SM (tensor memory, shared memory): K3d on
-                // k3d_sms SMs, K2 (HBM-bound) on the rest at the same time. K2 is K3d's
-                // programmatic dependent, launched once every K3d CTA holds its SM and has seen
-                // X complete, so its CTAs land on the free SMs; the consumer joins both.
-                if (!xg_done)
-                    prof(BD_PROF_XQ_PREP, s, [&] { mtd_gather_launch(X, ldx, cols, md.gat, md.prm.n_ten, p.xg, p.xg_ld, s); });
-                xg_done = false;
-                prof(BD_PROF_FUSED_QKV + group, s, [&] {
-                    MtdParams m2 = md.prm;
-                    m2.grid = std::min(m2.n_tasks, k3d_sms);
-                    mtd_launch(m2, s);
-                    BD_CUDA(cudaEventRecord(ev_fork, s));
-                    BD_CUDA(cudaStreamWaitEvent(stream2, ev_fork, 0));
-                    GemmPlan g2 = g;
-                    g2.grid = std::min(g.grid, (g.grid / kNumSMs) * (kNumSMs - m2.grid));
-                    g2.after_k3d = true;
-                    base_gemm(g2, l, group, mw, mx, stream2);
-                    BD_CUDA(cudaEventRecord(ev_join, stream2));
-                    BD_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
-                });
-                return;
-            }
-            // serial: K2, then K3d on every SM
             if (!xg_done)
                 prof(BD_PROF_XQ_PREP, s, [&] { mtd_gather_launch(X, ldx, cols, md.gat, md.prm.n_ten, p.xg, p.xg_ld, s); });
             xg_done = false;
