@@ -242,12 +242,14 @@ def _random_entries(arch, rng, alpha=2e-3, raw_sigma=1e-2):
     return ents
 
 
-def test_head_dim_128_long_context_matches_port(cuda, port):
-    """The head_dim-128 attention kernel (the Llama-2-7B shape) past its 192-row
-    shared-memory staging (two K/V chunks), two tenants, against the port on a
-    bf16 backbone."""
-    arch = dict(vocab=64, dim=256, n_layers=1, n_heads=2, intermediate=512, max_seq=220,
-                rope_theta=10000.0, kv_dim=256)
+@pytest.mark.parametrize("dim,n_heads,kv_dim", [(256, 2, 256), (512, 4, 256), (1024, 8, 256), (1024, 8, 128)])
+def test_head_dim_128_long_context_matches_port(cuda, port, dim, n_heads, kv_dim):
+    """The head_dim-128 attention kernels past their 192-row shared-memory staging (two K/V
+    chunks), two tenants, against the port on a bf16 backbone: multi-head (the Llama-2-7B
+    shape) and grouped-query with 2, 4 and 8 query heads per KV head (attn128g_kernel: one
+    CTA per request and KV head; Mistral-7B has 4, Llama-2-70B 8)."""
+    arch = dict(vocab=64, dim=dim, n_layers=1, n_heads=n_heads, intermediate=512, max_seq=220,
+                rope_theta=10000.0, kv_dim=kv_dim)
     rng = np.random.default_rng(7)
     tens = {}
     for name, r, c in tensor_shapes(arch):
