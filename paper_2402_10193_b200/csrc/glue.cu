@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kRnThreads)
     resid_norm_cluster_kernel(float* __restrict__ x, int dim, ProjOut proj, const float* const* __restrict__ norm_w,
                               uint16_t* __restrict__ xn, int ldxn, float* __restrict__ xn_f32, XgOut xo) {
     __shared__ double red_d[32];
-    __shared__ double part_sq;
+    __shared__ double part_sq[8];  // chunk k's sum of squares, pushed here by CTA k
     __shared__ double inv_s;
     const unsigned long long t_entry = gtimer();
     griddep_wait();  // PDL: the projection partials come from the previous kernel
@@ -276,25 +276,22 @@ __global__ void __launch_bounds__(kRnThreads)
     double sq = static_cast<double>(v.x) * v.x + static_cast<double>(v.y) * v.y +
                 static_cast<double>(v.z) * v.z + static_cast<double>(v.w) * v.w;
     sq = block_sum(sq, red_d);
-    if (threadIdx.x == 0) part_sq = sq;
     uint32_t rank;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    if (threadIdx.x < nc) {  // push this chunk's sum into slot `rank` of every CTA of the request
+        const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(&part_sq[rank]));
+        uint32_t remote;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(int(threadIdx.x)));
+        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(sq) : "memory");
+    }
+    // one cluster barrier: every push has landed, and no CTA touches another's memory after it
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     if (threadIdx.x == 0) {
         double msq = 0.0;
-        const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(&part_sq));
-        for (int k = 0; k < nc; ++k) {
-            uint32_t remote;
-            double pk;
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(k));
-            asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(pk) : "r"(remote) : "memory");
-            msq += pk;
-        }
+        for (int k = 0; k < nc; ++k) msq += part_sq[k];  // chunk order (same bits as before)
         inv_s = 1.0 / sqrt(msq / static_cast<double>(dim) + 1e-12);
     }
-    // no CTA leaves (its part_sq must stay readable) before every CTA has read the sums
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    (void)rank;
+    __syncthreads();
     if (!on) return;
     const double inv = inv_s;
     const float y0 = static_cast<float>(static_cast<double>(v.x) * inv) * w.x;
