@@ -170,11 +170,13 @@ void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stre
 // ---- K3d: tenants with many requests, dense tensor-core delta (mtd.cu) ----
 constexpr int kMtdMaxTenants = 8;
 constexpr int kMtdMaxN = 64;  // requests per tenant (MMA N, padded to 16)
-// the auto policy takes K3d from 16 requests per tenant at batch >= 64. Measured (tok/s):
-// M7 B=64 T=1 7 963 vs K23 5 089, T=4 (16/tenant) 6 272 vs 5 072, T=8 (8/tenant) 4 641 vs
-// K23 5 126; L7 B=16 T=1 (16/tenant) 2 807 vs the byte LUT 3 129 (its 16 jobs read one plane,
-// mostly from L2, and it runs beside K2 while K3d runs after it)
-constexpr double kMtdMinRequests = 16.0;
+// the auto policy takes K3d from 8 requests per tenant at batch >= 64. Measured (tok/s, M7 B=64,
+// round-2 build with grouped-query attention and K3d inputs written by their producers):
+// T=8 (8/tenant) K3d 5 280 vs K23 5 183-5 232; T=16 (4/tenant) K3d 4 763 vs K23 5 168; earlier:
+// T=1 K3d 7 963 vs K23 5 089, T=4 6 272 vs 5 072; L7 B=16 T=1 (16/tenant) K3d 2 807 vs the byte
+// LUT 3 129 (its 16 jobs read one plane, mostly from L2, and it runs beside K2 while K3d runs
+// after it)
+constexpr double kMtdMinRequests = 8.0;
 constexpr int kMtdMinBatch = 64;
 struct MtdTenant {
     std::vector<int> reqs;  // batch indices

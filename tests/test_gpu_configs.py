@@ -138,7 +138,7 @@ def test_config2_l7_stack_B16(cuda, port, tenants):
                       expect_paths="LLLL") <= 1e-2
 
 
-@pytest.mark.parametrize("tenants,paths", [(1, "DDDD"), (4, "DDDD"), (16, "TTTT"), (64, "LLLL")])
+@pytest.mark.parametrize("tenants,paths", [(1, "DDDD"), (4, "DDDD"), (8, "DDDD"), (16, "TTTT"), (64, "LLLL")])
 def test_config3_m7_gqa_B64(cuda, port, tenants, paths):
     """configs[3]: Mistral-7B GQA (kv_dim 1024 < dim), batch 64, tenant sweep through the
     default dispatch (K3d from 8 requests per tenant, K23 from 2, the byte LUT below)."""
