@@ -146,14 +146,18 @@ std::vector<float> packed_matvec(const PackedSignMatrix& p, std::span<const floa
 
 namespace {
 
-// device pool of one reference ServingPool object (keyed by its address; the fingerprint
-// and request count detect a new pool constructed at a recycled address)
+// device pool of one reference ServingPool object (keyed by its address). A new pool
+// constructed at a recycled address (e.g. a stack object in a loop, whose checkpoint copy may
+// even land on the same heap address) is detected by its requests: a request id decoding at a
+// position below the one this side already served it at cannot belong to the same pool (the
+// reference's positions only grow, serve.cpp validates position == cache length).
 struct GpuSide {
     bd_pool* pool = nullptr;
     const void* fingerprint = nullptr;
     size_t requests_seen = 0;
     std::set<std::string> tenants;
     std::map<size_t, uint64_t> rid;
+    std::map<size_t, size_t> next_pos;  // reference request id -> next position served
 };
 std::mutex g_m;
 std::map<const void*, GpuSide> g_side;
@@ -203,7 +207,12 @@ static std::vector<std::vector<float>> gpu_decode(const void* self, const ModelC
     std::lock_guard<std::mutex> lk(g_m);
     const void* fp = backbone.tensors.empty() ? nullptr : backbone.tensors.begin()->second.values().data();
     GpuSide& g = g_side[self];
-    if (g.pool && (g.fingerprint != fp || n_requests < g.requests_seen)) {  // recycled address
+    bool recycled = g.pool && (g.fingerprint != fp || n_requests < g.requests_seen);
+    for (const DecodeRequest& q : batch.requests) {
+        auto it = g.next_pos.find(q.request_id);
+        if (it != g.next_pos.end() && q.position < it->second) recycled = true;
+    }
+    if (recycled) {  // a new reference pool at a recycled address
         bd_pool_destroy(g.pool);
         g = GpuSide{};
     }
@@ -234,6 +243,7 @@ static std::vector<std::vector<float>> gpu_decode(const void* self, const ModelC
     }
     std::vector<float> logits(B * cfg.vocab);
     ok(bd_pool_decode_step(g.pool, reqs.data(), B, mode, logits.data(), nullptr));
+    for (const DecodeRequest& q : batch.requests) g.next_pos[q.request_id] = q.position + 1;
     std::vector<std::vector<float>> out(B);
     for (size_t r = 0; r < B; ++r) out[r].assign(logits.begin() + r * cfg.vocab, logits.begin() + (r + 1) * cfg.vocab);
     return out;
