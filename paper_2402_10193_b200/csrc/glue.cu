@@ -1026,11 +1026,15 @@ bool resid_norm_launch(float* x, int batch, int dim, const ProjOut& proj, const 
 bool attn_launch(const ProjOut& qkv, const AttnArgs& a, const int* pos_dev, int batch,
                  uint16_t* ctx, int ld_ctx, cudaStream_t s) {
     const int group = a.n_heads / a.n_kv_heads;
-    if (a.hd == 128 && a.kv_dim % 8 == 0 && a.dim % 8 == 0 && (group == 2 || group == 4 || group == 8)) {
+    const int g_rows = std::min(192, std::max(32, a.max_seq));
+    const size_t g_smem =
+        ((group + 2) * 128 + size_t(group) * a.max_seq) * sizeof(float) + size_t(g_rows) * 128 * 2;
+    // (score buffers of G heads too large for shared memory: one CTA per query head below)
+    if (a.hd == 128 && a.kv_dim % 8 == 0 && a.dim % 8 == 0 && (group == 2 || group == 4 || group == 8) &&
+        g_smem <= 220 * 1024) {
         // grouped-query heads: one CTA per (request, KV head), K / V staged once for the group
-        const int rows = std::min(192, std::max(32, a.max_seq));
-        const size_t smem = ((group + 2) * 128 + size_t(group) * a.max_seq) * sizeof(float) + size_t(rows) * 128 * 2;
-        require(smem <= 220 * 1024, BD_ERR_BAD_ARGUMENT, "attention: max_seq too large for the score buffer");
+        const int rows = g_rows;
+        const size_t smem = g_smem;
         static bool attr[3] = {false, false, false};
         auto launch = [&](auto kern, int gi) {
             if (!attr[gi]) {

@@ -282,6 +282,38 @@ def test_head_dim_128_long_context_matches_port(cuda, port, dim, n_heads, kv_dim
     pool.close()
 
 
+def test_gqa_long_max_seq_uses_per_head_attention(cuda, port):
+    """Grouped-query heads whose G score buffers do not fit in shared memory (8 query heads per
+    KV head at max_seq 7000) fall back to one CTA per query head instead of failing."""
+    arch = dict(vocab=64, dim=1024, n_layers=1, n_heads=8, intermediate=512, max_seq=7000,
+                rope_theta=10000.0, kv_dim=128)
+    rng = np.random.default_rng(11)
+    tens = {}
+    for name, r, c in tensor_shapes(arch):
+        w = rng.standard_normal((r, c)).astype(np.float32) * (1.0 if r == 1 else 0.05)
+        tens[name] = bf16_round(w + (1.0 if r == 1 else 0.0))
+    pool = ServingPool(arch, tens)
+    ents = [_random_entries(arch, rng) for _ in range(2)]
+    for t, e in enumerate(ents):
+        pool.register_delta_entries(f"t{t}", e)
+    rids = [pool.open_request(f"t{t}") for t in range(2)]
+    names = [n for n, _, _ in tensor_shapes(arch)]
+    port_ents = [[{k: v for k, v in e.items()} for e in es] for es in ents]
+    for es in port_ents:
+        for e in es:
+            if e["kind"] == "raw":
+                e["raw"] = e["raw"].reshape(-1)
+    flat = np.concatenate([tens[n].reshape(-1) for n in names])
+    kc = [np.zeros((1, arch["max_seq"], arch["kv_dim"]), np.float32) for _ in range(2)]
+    vc = [np.zeros_like(k) for k in kc]
+    for pos, tok in enumerate(rng.integers(0, arch["vocab"], 4)):
+        got = pool.decode_step([(r, int(tok), pos) for r in rids])
+        want = port.decode(arch, flat, port_ents, [0, 1], [int(tok)] * 2, [pos] * 2, kc, vc)
+        for i in range(2):
+            assert rel_l2(got[i], want[i]) <= 2e-2, (pos, i, rel_l2(got[i], want[i]))
+    pool.close()
+
+
 def _k23_pool_run(port, B_per_t, steps, n_tenants=2, dim=256, inter=512, n_layers=2):
     """n_tenants tenants x B_per_t requests each on a 128-multiple shape (K23-eligible),
     several decode steps against the port on the same bf16 backbone."""
