@@ -159,6 +159,7 @@ struct LutJob {
 };
 struct LutParams {
     int n_jobs, slices, cols, ldx, batch, M, n_segs, grid;
+    int ld_u4;  // plane row stride in 16-byte words (v2 kernel): cols / 128, or the pool's padded rows
     int seg_row0[kLutMaxSegs + 1];  // stacked row offsets of the sub-matrices
     LutJob jobs[kLutMaxJobs];
 };

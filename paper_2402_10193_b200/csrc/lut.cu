@@ -255,7 +255,7 @@ __device__ __forceinline__ void build_tables_v2(float* T, const float* xs, int t
         for (int el = 0; el < 16; ++el) Tw[((quarter * 4 + eh) * 16 + el) * 64] = hi[eh] + lo[el];
 }
 
-template <int kWPR>  // words per plane row (cols/32); 0 = runtime value
+template <int kWPR, int kLdU4 = kWPR / 4>  // words per plane row (cols/32), row stride in 16-B words; 0 = runtime
 __global__ void __maxnreg__(kLutRegs)
     lut2_kernel(const __grid_constant__ LutParams p, const uint16_t* __restrict__ X,
                 float* __restrict__ out) {
@@ -342,7 +342,7 @@ __global__ void __maxnreg__(kLutRegs)
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         const int r = min(r0 + 4 * grp + i, lb - 1);
-                        w[i] = ld_plane(plane + static_cast<size_t>(r) * (wpr / 4));
+                        w[i] = ld_plane(plane + static_cast<size_t>(r) * (kLdU4 ? kLdU4 : p.ld_u4));
                     }
                 };
                 auto consume = [&](int r0, const uint4 (&wc)[4]) {
@@ -426,6 +426,7 @@ bool plan_lut(LutParams& p, const int* seg_rows, int n_segs, int cols, int ldx, 
     p.ldx = ldx;
     p.batch = batch;
     p.slices = (cols + kSliceCols - 1) / kSliceCols;
+    p.ld_u4 = cols / 128;  // flat reference layout (v2 needs cols % 128 == 0)
     p.n_segs = n_segs;
     int total = 0;
     for (int s = 0; s < n_segs; ++s) {
@@ -459,21 +460,21 @@ void lut_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t st
                        static_cast<const uint16_t*>(X), out));
 }
 
-template <int kWPR>
+template <int kWPR, int kLdU4 = kWPR / 4>
 void lut2_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t stream) {
     static bool attr = false;
     if (!attr) {
-        BD_CUDA(cudaFuncSetAttribute(lut2_kernel<kWPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        BD_CUDA(cudaFuncSetAttribute(lut2_kernel<kWPR, kLdU4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(kLut2Smem)));
         // max carveout (K2 co-resident on every SM) where plane rows are 128-B aligned; the
         // down projection (1376-B rows) measured faster on the default carveout, K2 after
         // it (profiles/r02_exp_down_carveout.txt: 1.487 vs 1.857 ms/step for down)
         if (kWPR % 32 == 0 && kWPR > 0)
-            BD_CUDA(cudaFuncSetAttribute(lut2_kernel<kWPR>, cudaFuncAttributePreferredSharedMemoryCarveout,
+            BD_CUDA(cudaFuncSetAttribute(lut2_kernel<kWPR, kLdU4>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          int(cudaSharedmemCarveoutMaxShared)));
         attr = true;
     }
-    BD_CUDA(launch_pdl(lut2_kernel<kWPR>, dim3(p.grid), dim3(kLutThreads), kLut2Smem, stream, p,
+    BD_CUDA(launch_pdl(lut2_kernel<kWPR, kLdU4>, dim3(p.grid), dim3(kLutThreads), kLut2Smem, stream, p,
                        static_cast<const uint16_t*>(X), out));
 }
 
@@ -488,13 +489,17 @@ static bool lut2_ok(const LutParams& p) {
 
 void lut_launch(const LutParams& p, const void* X, float* out, cudaStream_t stream) {
     if (lut2_ok(p)) {
-        switch (p.cols) {
+        // the row stride is a compile-time constant on the hot shapes (an immediate in every
+        // plane address; a runtime stride costs the issue-bound loop ~15 %)
+        const bool flat = p.ld_u4 == p.cols / 128;
+        switch (flat ? p.cols : (p.cols == 11008 && p.ld_u4 == 88 ? -11008 : 0)) {
             case 4096: lut2_launch_t<128>(p, X, out, stream); break;
             case 8192: lut2_launch_t<256>(p, X, out, stream); break;
             case 11008: lut2_launch_t<344>(p, X, out, stream); break;
+            case -11008: lut2_launch_t<344, 88>(p, X, out, stream); break;  // pool: 1 408-B padded rows
             case 14336: lut2_launch_t<448>(p, X, out, stream); break;
             case 28672: lut2_launch_t<896>(p, X, out, stream); break;
-            default: lut2_launch_t<0>(p, X, out, stream); break;
+            default: lut2_launch_t<0, 0>(p, X, out, stream); break;
         }
         note_launch();
         BD_CUDA(cudaGetLastError());

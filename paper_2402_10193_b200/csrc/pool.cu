@@ -106,7 +106,16 @@ T* dmalloc(size_t n, std::vector<void*>* owner = nullptr) {
 struct Plane {
     const uint8_t* bits;
     float alpha;
+    // the same rows padded to a multiple of 128 bytes for the byte-LUT (rows of 11 008 columns
+    // are 1 376 B: 3 of 4 row slices would straddle two L2 lines); null where rows are aligned
+    const uint8_t* bits_lut = nullptr;
+    int ld_lut = 0;  // bytes per padded row
 };
+// LUT row padding: 128-B multiples where the rows are long and not already aligned
+inline uint64_t lut_row_bytes(uint64_t cols) {
+    const uint64_t b = cols / 8;
+    return (cols % 128 == 0 && b > 128 && b % 128 != 0) ? (b + 127) / 128 * 128 : 0;
+}
 
 struct Tenant {
     std::string id, path;
@@ -639,7 +648,15 @@ struct PoolImpl {
             BD_CUDA(cudaMemset(d, 0, round_up(len, 16)));
             BD_CUDA(cudaMemcpy(d, e.bits + k * nb + b0, len,
                                e.is_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
-            out.push_back({d, e.scales[k]});
+            Plane pl{d, e.scales[k]};
+            if (const uint64_t ld = lut_row_bytes(e.cols)) {  // padded copy for the LUT (+2.3 % at 11 008)
+                uint8_t* q = dmalloc<uint8_t>(nr * ld, &t.allocs);
+                BD_CUDA(cudaMemset(q, 0, nr * ld));
+                BD_CUDA(cudaMemcpy2D(q, ld, d, e.cols / 8, e.cols / 8, nr, cudaMemcpyDeviceToDevice));
+                pl.bits_lut = q;
+                pl.ld_lut = int(ld);
+            }
+            out.push_back(pl);
         }
         return out;
     }
@@ -860,6 +877,7 @@ struct PoolImpl {
                 seg_rows[s] = int(nr);
             }
             bool ok = true;
+            const uint64_t lut_ld = lut_row_bytes(gd.cols);
             for (uint64_t l = 0; l < nL && ok; ++l) {
                 for (int b0 = 0; b0 < B && ok; b0 += kLutMaxJobs) {
                     LutParams prm{};
@@ -872,12 +890,14 @@ struct PoolImpl {
                             const auto& planes = t.proj[l][gd.projs[s]];
                             j.n_planes[s] = int(planes.size());
                             for (size_t k = 0; k < planes.size(); ++k) {
-                                j.bits[s][k] = planes[k].bits;
+                                // the padded rows where the pool keeps them (lut_row_bytes)
+                                j.bits[s][k] = lut_ld ? planes[k].bits_lut : planes[k].bits;
                                 j.alpha[s][k] = planes[k].alpha;
                             }
                         }
                     }
                     ok = plan_lut(prm, seg_rows, int(gd.projs.size()), int(gd.cols), int(gd.ldx), B);
+                    if (ok && lut_ld) prm.ld_u4 = int(lut_ld / 16);
                     if (ok && size_t(prm.slices) * B * prm.M > D_elems) ok = false;
                     if (ok) p.lut[l][gi].prm.push_back(prm);
                 }
