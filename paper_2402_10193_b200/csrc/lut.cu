@@ -466,10 +466,12 @@ void lut2_launch_t(const LutParams& p, const void* X, float* out, cudaStream_t s
     if (!attr) {
         BD_CUDA(cudaFuncSetAttribute(lut2_kernel<kWPR, kLdU4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(kLut2Smem)));
-        // max carveout (K2 co-resident on every SM) where plane rows are 128-B aligned; the
-        // down projection (1376-B rows) measured faster on the default carveout, K2 after
-        // it (profiles/r02_exp_down_carveout.txt: 1.487 vs 1.857 ms/step for down)
-        if (kWPR % 32 == 0 && kWPR > 0)
+        // max carveout (K2 co-resident on every SM) where the plane rows are 128-B aligned,
+        // which includes the pool's padded down-projection rows (1 408 B: down phase 1.49 ->
+        // 1.30 ms/step, profiles/r02_exp_lut_down_padded_rows_ab.txt); unaligned rows (the
+        // reference's 1 376 B) ran faster on the default carveout with K2 after the LUT
+        // (profiles/r02_exp_down_carveout.txt)
+        if (kLdU4 % 8 == 0 && kLdU4 > 0)
             BD_CUDA(cudaFuncSetAttribute(lut2_kernel<kWPR, kLdU4>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          int(cudaSharedmemCarveoutMaxShared)));
         attr = true;
